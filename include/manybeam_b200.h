@@ -1,0 +1,204 @@
+/*
+ * manybeam_b200 — C-ABI of the B200-native forward model (matrix-ODE
+ * propagation + RHST + surface boundary solve -> rocking-curve intensities).
+ *
+ * Drop-in boundary for the reference C++ library `manybeam`
+ * (/root/reference/proj, arXiv 2306.00271). Every entry point names the
+ * reference interface it replaces. Plain C types only: no torch, no C++, no
+ * exceptions across the ABI. All arithmetic on the device path is FP64
+ * (complex128 as interleaved re/im doubles, layout-compatible with
+ * std::complex<double> / cuDoubleComplex).
+ *
+ * Error model (reference types.hpp:20-62 -> status codes): every function
+ * returns MB_OK or one of the MB_ERR_* codes below; mb_last_error() returns a
+ * thread-local message. Per-point failures (BreakdownError with a step index)
+ * are reported in mb_point_status; the first failing point in row order
+ * decides the call's return code, as the reference rethrows worker errors in
+ * row order (sweep.cpp:136-137).
+ *
+ * There is NO CPU fallback: without a usable sm_100 device every solve
+ * returns MB_ERR_CUDA.
+ */
+#ifndef MANYBEAM_B200_H
+#define MANYBEAM_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (types.hpp:20-62) ---------------------------------- */
+#define MB_OK 0
+#define MB_ERR_CONFIG 1      /* ConfigError */
+#define MB_ERR_SOLVER 2      /* SolverError (generic) */
+#define MB_ERR_SINGULAR 3    /* SingularMatrixError */
+#define MB_ERR_BREAKDOWN 4   /* BreakdownError{step} */
+#define MB_ERR_CONVERGENCE 5 /* ConvergenceError */
+#define MB_ERR_DOMAIN 6      /* DomainError */
+#define MB_ERR_CUDA 7        /* device / runtime failure, no device */
+#define MB_ERR_ARG 8         /* null pointer, bad size, capacity too small */
+
+/* per-point breakdown causes (proposed.cpp:280-287, 303-308) */
+#define MB_POINT_OK 0
+#define MB_POINT_NONFINITE 1   /* "propagation state went nonfinite" */
+#define MB_POINT_RHST 2        /* "stabilizing transform: ..." (zero pivot or residual > 1e-10) */
+#define MB_POINT_EXTRACTION 3  /* "reflection extraction: ..." (zero pivot) */
+
+typedef struct mb_context mb_context;
+typedef struct mb_plan mb_plan;
+
+/* ---- geometry / rods (rods.hpp:9-47, rods.cpp:14-96) ------------------ */
+typedef struct {
+  double a1[2]; /* direct basis, A */
+  double a2[2];
+} mb_lattice;
+
+/* Rod set in the reference order (||k||, kx, ky), zero rod first, plus the
+ * deduplicated difference table. Caller-owned arrays:
+ *   k[n][2] (1/A), m[n][2], diff[ndiff][2] (1/A), diff_m[ndiff][2],
+ *   diff_index[n*n] with diff_index[j*n+k] = index of k_j - k_k (rods.hpp:37). */
+typedef struct {
+  int n;
+  const double* k;
+  const int* m;
+  int ndiff;
+  const double* diff;
+  const int* diff_m;
+  const int* diff_index;
+} mb_rods;
+
+/* RodSet::build (rods.cpp:32-96) when first_n <= 0; otherwise the first-N
+ * truncation of the same order (EXTENSION, SURVEY.md finding 4; `cutoff` is
+ * ignored). Two-call pattern: with null output arrays only *n and *ndiff are
+ * written; with arrays of capacity cap_n / cap_diff they are filled.
+ * Returns MB_ERR_ARG when a capacity is too small (sizes still written). */
+int mb_rods_build(const mb_lattice* lattice, double cutoff, int first_n, int* n, int* ndiff,
+                  double* k, int* m, double* diff, int* diff_m, int* diff_index, int cap_n,
+                  int cap_diff);
+
+/* ---- potential fields (potential.hpp:11-61) --------------------------- */
+#define MB_FIELD_ZERO 0
+#define MB_FIELD_GAUSSIAN_LAYERS 1 /* GaussianLayer list, potential.hpp:17-23 */
+#define MB_FIELD_TABULATED 2       /* cubic-Hermite table, potential.cpp:169-199 */
+#define MB_FIELD_ATOMS 3           /* EXTENSION: atoms + 4-Gaussian form factors */
+
+typedef struct {
+  int kind;
+  double z_bottom; /* A, < 0 */
+  int has_bulk_period; /* bulk seeding is the §8f "next" row: rejected for now */
+  double bulk_period;
+  /* MB_FIELD_GAUSSIAN_LAYERS: layers[nlayers][5] = z_center, amplitude,
+   * sigma_xy, sigma_z, absorption */
+  int nlayers;
+  const double* layers;
+  /* MB_FIELD_TABULATED: z_grid[ngrid]; entry_dm[nentries][2];
+   * entry_values[nentries][ngrid][2] (re, im) */
+  int ngrid;
+  const double* z_grid;
+  int nentries;
+  const int* entry_dm;
+  const double* entry_values;
+  /* MB_FIELD_ATOMS: atom_xyz[natoms][3] Cartesian A, atom_species[natoms],
+   * atom_B[natoms] (Debye-Waller, A^2); ff_a/ff_b[nspecies][4] (A, A^2).
+   * u(dg, z) = (particle_sign - i*absorption) * gamma_L * (4 pi / cell_area)
+   *   * sum_a e^{-i dg.rho_a} sum_i a_i (2 sqrt(pi)/sqrt(b')) e^{-b'|dg|^2/16pi^2}
+   *   * e^{-4 pi^2 (z - z_a)^2 / b'},  b' = b_i + B_a */
+  int natoms;
+  const double* atom_xyz;
+  const int* atom_species;
+  const double* atom_B;
+  int nspecies;
+  const double* ff_a;
+  const double* ff_b;
+  double cell_area;
+  double gamma_L;
+  double particle_sign; /* +1 electron, -1 positron */
+  double absorption;
+} mb_field;
+
+/* EXTENSION: relativistic beam from kinetic energy (eV):
+ * gamma = 2 pi / lambda (1/A), gamma_L = 1 + E / m0 c^2. */
+int mb_beam_from_energy(double energy_ev, double* gamma, double* gamma_L);
+
+/* ---- stepper (proposed.hpp:23-43, splitting_coefficients.cpp) -------- */
+#define MB_STEP_RK4 0
+#define MB_STEP_SPLITTING 1
+#define MB_SPLIT_ABA 0
+#define MB_SPLIT_BAB 1
+typedef struct {
+  int algorithm;
+  int variant;
+  int ndrift;
+  const double* drift;
+  int nkick;
+  const double* kick;
+} mb_stepper;
+
+/* StepperSpec::by_name (proposed.cpp:24-29): "rk4", "sp4", "sp6". The
+ * coefficient arrays point to library-owned static storage. */
+int mb_stepper_by_name(const char* name, mb_stepper* out);
+
+/* ---- solve options (sweep.hpp:26-32, proposed.hpp:90-92) --------------- */
+typedef struct {
+  double dz;             /* target slice width, SlicingPlan::with_target_dz */
+  long slices;           /* EXTENSION: >0 fixes the count (SlicingPlan::with_count) */
+  double rhst_threshold; /* strict '>' trigger, +inf disables (proposed.cpp:198) */
+  int residual_check;    /* 1: solve_right's 1e-10 residual gate on every RHST (kernels.cpp:75-79) */
+  int fsal;              /* 1: merge the last kick of a step with the next step's first
+                            (same node height; exact in exact arithmetic). 0 = reference op order */
+} mb_options;
+
+/* one (structure, glancing angle) point */
+typedef struct {
+  int structure;
+  double theta0_deg;
+  double theta1_deg;
+} mb_pair;
+
+typedef struct {
+  int code;        /* MB_POINT_* */
+  int step;        /* BreakdownError::step */
+  int rhst_count;  /* SolveStats::rhst_transforms */
+  int reserved;
+} mb_point_status;
+
+/* ---- context ----------------------------------------------------------- */
+/* One context per device; owns streams and a grow-only device arena reused
+ * across calls. Thread-safe per context (calls serialize on an internal lock). */
+int mb_context_create(int device, mb_context** out);
+int mb_context_destroy(mb_context* ctx);
+const char* mb_last_error(void);
+/* 1 when the library was built for sm_100a and a matching device is present */
+int mb_device_ok(int device);
+
+/* ---- batched solve (plan / execute split, cuFFT-style) ----------------
+ * Replaces the per-row loop of rocking_curve (sweep.cpp:89-138) with one
+ * device pass over all (structure, angle) pairs. Every field shares one rod
+ * set, gamma, z_bottom and slicing. */
+int mb_plan_create(mb_context* ctx, const mb_rods* rods, const mb_field* fields, int nfields,
+                   double gamma, const mb_pair* pairs, long npairs, const mb_stepper* stepper,
+                   const mb_options* opts, mb_plan** out);
+/* K1 (slice-potential coefficients) + K2 (propagation, RHST, extraction,
+ * intensity). Inputs already device-resident; stream 0 = context stream. */
+int mb_plan_execute(mb_plan* plan, void* cuda_stream);
+/* D2H of eta[npairs][n], optional rho[npairs][n][2], optional status[npairs].
+ * Returns the first failing pair's code (row order). */
+int mb_plan_results(mb_plan* plan, double* eta, double* rho, mb_point_status* status);
+/* timing of the last execute (CUDA events on the execute stream): total,
+ * potential kernel, propagation kernel, in milliseconds; kernel launches */
+int mb_plan_timing(const mb_plan* plan, double* ms_total, double* ms_potential,
+                   double* ms_propagate, int* launches);
+/* number of node slots of the coefficient table and its device bytes */
+int mb_plan_info(const mb_plan* plan, long* slots, int* ndiff, long* coef_bytes, int* npad);
+int mb_plan_destroy(mb_plan* plan);
+
+/* rocking_curve (sweep.hpp:37-38, sweep.cpp:54-143), stepper methods:
+ * rows are theta1-major with theta0 inner (sweep.cpp:90-91). eta[rows][n]. */
+int mb_rocking_curve(mb_context* ctx, const mb_field* field, const mb_rods* rods, double gamma,
+                     const double* theta0, int n_theta0, const double* theta1, int n_theta1,
+                     const mb_stepper* stepper, const mb_options* opts, double* eta, double* rho,
+                     mb_point_status* status);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MANYBEAM_B200_H */

@@ -1,0 +1,953 @@
+// Host runtime of the B200-native forward model: the C-ABI of
+// include/manybeam_b200.h. Host-side logic restates the reference's setup
+// layers (rods, beam geometry, slicing, node schedules, stepper tables;
+// /root/reference/proj/core/src/{rods,geometry,stages,proposed,
+// splitting_coefficients}.cpp) and stages every input on the device once per
+// plan; all per-slice arithmetic runs in the sm_100a kernels (mb_kernels.cu).
+// There is no CPU solve path: without a device every solve fails with
+// MB_ERR_CUDA.
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <limits>
+#include <map>
+#include <mutex>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/manybeam_b200.h"
+#include "mb_internal.h"
+
+namespace {
+
+using cd = std::complex<double>;
+constexpr double kPi = 3.14159265358979323846;
+constexpr double kTwoPi = 2.0 * kPi;
+constexpr double kDegToRad = kPi / 180.0;
+
+thread_local std::string g_last_error;
+
+struct MbError : std::runtime_error {
+  int code;
+  MbError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] void fail(int code, const std::string& msg) { throw MbError(code, msg); }
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(MB_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    g_last_error.clear();
+    return MB_OK;
+  } catch (const MbError& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "out of host memory";
+    return MB_ERR_CUDA;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return MB_ERR_SOLVER;
+  }
+}
+
+// ------------------------------------------------------------------ rods
+// rods.cpp:14-96 (+ first-N extension)
+struct V2 {
+  double x, y;
+};
+struct Rod {
+  V2 k;
+  int m1, m2;
+};
+double vnorm(V2 v) { return std::sqrt(v.x * v.x + v.y * v.y); }
+
+struct Lattice {
+  V2 a1, a2;
+  V2 b1() const {
+    const double det = a1.x * a2.y - a1.y * a2.x;
+    return V2{kTwoPi * a2.y / det, -kTwoPi * a2.x / det};
+  }
+  V2 b2() const {
+    const double det = a1.x * a2.y - a1.y * a2.x;
+    return V2{-kTwoPi * a1.y / det, kTwoPi * a1.x / det};
+  }
+  void validate() const {
+    const double det = a1.x * a2.y - a1.y * a2.x;
+    const double scale = vnorm(a1) * vnorm(a2);
+    if (!(std::abs(det) > 1e-12 * std::max(scale, 1e-300)))
+      fail(MB_ERR_CONFIG, "lattice: basis vectors are degenerate (zero cell area)");
+    if (!std::isfinite(a1.x) || !std::isfinite(a1.y) || !std::isfinite(a2.x) || !std::isfinite(a2.y))
+      fail(MB_ERR_CONFIG, "lattice: nonfinite basis");
+  }
+};
+
+std::vector<Rod> enumerate_rods(const Lattice& lat, double cutoff) {
+  const V2 b1 = lat.b1(), b2 = lat.b2();
+  const int m1max = (int)std::floor(cutoff * vnorm(lat.a1) / kTwoPi + 1e-9);
+  const int m2max = (int)std::floor(cutoff * vnorm(lat.a2) / kTwoPi + 1e-9);
+  std::vector<Rod> rods;
+  for (int m1 = -m1max; m1 <= m1max; ++m1)
+    for (int m2 = -m2max; m2 <= m2max; ++m2) {
+      const V2 k{m1 * b1.x + m2 * b2.x, m1 * b1.y + m2 * b2.y};
+      if (vnorm(k) <= cutoff) rods.push_back(Rod{k, m1, m2});
+    }
+  std::sort(rods.begin(), rods.end(), [](const Rod& p, const Rod& q) {
+    const double np = vnorm(p.k), nq = vnorm(q.k);
+    if (np != nq) return np < nq;
+    if (p.k.x != q.k.x) return p.k.x < q.k.x;
+    return p.k.y < q.k.y;
+  });
+  return rods;
+}
+
+struct RodTables {
+  std::vector<Rod> rods;
+  std::vector<V2> diff;
+  std::vector<std::pair<int, int>> diff_m;
+  std::vector<int> diff_index;
+};
+
+RodTables build_rods(const Lattice& lat, double cutoff, int first_n) {
+  lat.validate();
+  std::vector<Rod> rods;
+  if (first_n > 0) {
+    const double bmin = std::min(vnorm(lat.b1()), vnorm(lat.b2()));
+    double c = 0.5 * bmin;
+    for (;;) {
+      rods = enumerate_rods(lat, c);
+      if ((int)rods.size() >= first_n) break;
+      c *= 1.25;
+    }
+    rods.resize((std::size_t)first_n);
+  } else {
+    if (!(cutoff > 0.0) || !std::isfinite(cutoff)) fail(MB_ERR_CONFIG, "rod cutoff must be positive and finite");
+    rods = enumerate_rods(lat, cutoff);
+  }
+  if (rods.empty() || rods.front().m1 != 0 || rods.front().m2 != 0)
+    fail(MB_ERR_CONFIG, "rod set does not contain the zero rod");
+  RodTables t;
+  t.rods = rods;
+  const int n = (int)rods.size();
+  const V2 b1 = lat.b1(), b2 = lat.b2();
+  std::map<std::pair<int, int>, int> seen;
+  t.diff_index.assign((std::size_t)n * n, -1);
+  for (int j = 0; j < n; ++j)
+    for (int k = 0; k < n; ++k) {
+      const int d1 = rods[j].m1 - rods[k].m1, d2 = rods[j].m2 - rods[k].m2;
+      auto key = std::make_pair(d1, d2);
+      auto it = seen.find(key);
+      int d;
+      if (it == seen.end()) {
+        d = (int)t.diff.size();
+        seen.emplace(key, d);
+        t.diff.push_back(V2{d1 * b1.x + d2 * b2.x, d1 * b1.y + d2 * b2.y});
+        t.diff_m.push_back(key);
+      } else {
+        d = it->second;
+      }
+      t.diff_index[(std::size_t)j * n + k] = d;
+    }
+  return t;
+}
+
+// ------------------------------------------------------------------ steppers
+// splitting_coefficients.cpp:13-77 (published constants; trailing entries by
+// symmetry and the sum rule)
+struct Tables {
+  double sp4_drift[6], sp4_kick[7], sp6_drift[11], sp6_kick[12];
+  Tables() {
+    const double b1 = 0.0829844064174052, b2 = 0.396309801498368, b3 = -0.0390563049223486;
+    const double b4 = 1.0 - 2.0 * (b1 + b2 + b3);
+    const double a1 = 0.245298957184271, a2 = 0.604872665711080;
+    const double a3 = 0.5 - (a1 + a2);
+    const double d4[6] = {a1, a2, a3, a3, a2, a1};
+    const double k4[7] = {b1, b2, b3, b4, b3, b2, b1};
+    std::memcpy(sp4_drift, d4, sizeof d4);
+    std::memcpy(sp4_kick, k4, sizeof k4);
+    const double c1 = 0.0414649985182624, c2 = 0.198128671918067, c3 = -0.0400061921041533;
+    const double c4 = 0.0752539843015807, c5 = -0.0115113874206879;
+    const double c6 = 0.5 - (c1 + c2 + c3 + c4 + c5);
+    const double e1 = 0.123229775946271, e2 = 0.290553797799558, e3 = -0.127049212625417;
+    const double e4 = -0.246331761062075, e5 = 0.357208872795928;
+    const double e6 = 1.0 - 2.0 * (e1 + e2 + e3 + e4 + e5);
+    const double d6[11] = {e1, e2, e3, e4, e5, e6, e5, e4, e3, e2, e1};
+    const double k6[12] = {c1, c2, c3, c4, c5, c6, c6, c5, c4, c3, c2, c1};
+    std::memcpy(sp6_drift, d6, sizeof d6);
+    std::memcpy(sp6_kick, k6, sizeof k6);
+  }
+};
+const Tables& tables() {
+  static const Tables t;
+  return t;
+}
+
+// proposed.cpp:36-60
+void validate_stepper(const mb_stepper& s) {
+  if (s.algorithm == MB_STEP_RK4) return;
+  if (s.algorithm != MB_STEP_SPLITTING) fail(MB_ERR_CONFIG, "stepper: unknown algorithm");
+  const int nd = s.ndrift, nk = s.nkick;
+  const bool shape_ok = s.variant == MB_SPLIT_BAB ? (nk == nd + 1) : (nd == nk + 1);
+  if (nd <= 0 || nk <= 0 || !shape_ok || !s.drift || !s.kick)
+    fail(MB_ERR_CONFIG, "stepper: BAB needs s drifts and s+1 kicks, ABA the reverse");
+  double sa = 0.0, sb = 0.0;
+  for (int i = 0; i < nd; ++i) {
+    if (!std::isfinite(s.drift[i])) fail(MB_ERR_CONFIG, "stepper: nonfinite drift coefficient");
+    sa += s.drift[i];
+  }
+  for (int i = 0; i < nk; ++i) {
+    if (!std::isfinite(s.kick[i])) fail(MB_ERR_CONFIG, "stepper: nonfinite kick coefficient");
+    sb += s.kick[i];
+  }
+  if (std::abs(sa - 1.0) > 1e-13 || std::abs(sb - 1.0) > 1e-13)
+    fail(MB_ERR_CONFIG, "stepper: drift and kick coefficients must each sum to 1");
+  if (nk > mbx::kMaxOcc) fail(MB_ERR_CONFIG, "stepper: too many stages for the device kernel");
+}
+
+// stages.cpp:12-23
+std::vector<double> schedule_from_fracs(std::vector<double> raw) {
+  for (double& f : raw) {
+    if (std::abs(f) < 1e-12) f = 0.0;
+    if (std::abs(f - 1.0) < 1e-12) f = 1.0;
+  }
+  std::sort(raw.begin(), raw.end());
+  std::vector<double> u;
+  for (double f : raw)
+    if (u.empty() || f - u.back() > 1e-12) u.push_back(f);
+  return u;
+}
+
+// node schedule + kick occurrence -> node (proposed.cpp:62-100, stages.cpp:10)
+struct Schedule {
+  std::vector<double> frac;
+  std::vector<int> occ2node;
+  bool endpoint_pair() const { return frac.size() >= 2 && frac.front() == 0.0 && frac.back() == 1.0; }
+};
+Schedule make_schedule(const mb_stepper& s) {
+  Schedule sc;
+  if (s.algorithm == MB_STEP_RK4) {
+    sc.frac = {0.0, 0.5, 1.0};
+    sc.occ2node = {0, 1, 1, 2};  // RK4 stages: foot, mid, mid, top
+    return sc;
+  }
+  std::vector<double> fr;
+  double c = 0.0;
+  if (s.variant == MB_SPLIT_BAB) {
+    fr.push_back(0.0);
+    for (int i = 0; i < s.ndrift; ++i) {
+      c += s.drift[i];
+      fr.push_back(c);
+    }
+  } else {
+    for (int r = 0; r < s.nkick; ++r) {
+      c += s.drift[r];
+      fr.push_back(c);
+    }
+  }
+  sc.frac = schedule_from_fracs(fr);
+  for (double raw : fr) {
+    double f = raw;
+    if (std::abs(f) < 1e-12) f = 0.0;
+    if (std::abs(f - 1.0) < 1e-12) f = 1.0;
+    int best = 0;
+    double dist = std::numeric_limits<double>::infinity();
+    for (int m = 0; m < (int)sc.frac.size(); ++m) {
+      const double d = std::abs(sc.frac[m] - f);
+      if (d < dist) {
+        dist = d;
+        best = m;
+      }
+    }
+    sc.occ2node.push_back(best);
+  }
+  return sc;
+}
+
+// ------------------------------------------------------------------ fields
+// potential.cpp:17-88 validation (+ atoms extension)
+void validate_field(const mb_field& f) {
+  if (!(f.z_bottom < 0.0) || !std::isfinite(f.z_bottom))
+    fail(MB_ERR_CONFIG, "potential: z_bottom must be negative and finite");
+  if (f.has_bulk_period)
+    fail(MB_ERR_CONFIG, "potential: bulk-period seeding (compute_bulk_reflection_proposed) is not supported on the device path yet");
+  switch (f.kind) {
+    case MB_FIELD_ZERO:
+      return;
+    case MB_FIELD_GAUSSIAN_LAYERS:
+      if (f.nlayers < 0 || (f.nlayers > 0 && !f.layers)) fail(MB_ERR_ARG, "potential: layers missing");
+      for (int i = 0; i < f.nlayers; ++i) {
+        const double* l = f.layers + 5 * i;
+        bool fin = true;
+        for (int q = 0; q < 5; ++q) fin = fin && std::isfinite(l[q]);
+        if (!fin || !(l[2] > 0.0) || !(l[3] > 0.0) || l[4] < 0.0)
+          fail(MB_ERR_CONFIG, "potential: layer " + std::to_string(i) +
+                                  " needs sigma_xy > 0, sigma_z > 0, absorption >= 0, finite values");
+      }
+      return;
+    case MB_FIELD_TABULATED: {
+      if (f.ngrid < 2 || !f.z_grid) fail(MB_ERR_CONFIG, "potential: tabulated z_grid needs at least 2 points");
+      for (int i = 0; i + 1 < f.ngrid; ++i)
+        if (!(f.z_grid[i] < f.z_grid[i + 1]))
+          fail(MB_ERR_CONFIG, "potential: tabulated z_grid must be strictly increasing");
+      if (f.z_grid[0] > f.z_bottom + 1e-9 || f.z_grid[f.ngrid - 1] < -1e-9)
+        fail(MB_ERR_CONFIG, "potential: tabulated z_grid must cover [z_bottom, 0]");
+      for (long i = 0; i < (long)f.nentries * f.ngrid * 2; ++i)
+        if (!std::isfinite(f.entry_values[i])) fail(MB_ERR_CONFIG, "potential: tabulated entry has nonfinite sample");
+      return;
+    }
+    case MB_FIELD_ATOMS:
+      if (!(f.cell_area > 0.0)) fail(MB_ERR_CONFIG, "atoms: cell area must be positive");
+      if (!(f.absorption >= 0.0)) fail(MB_ERR_CONFIG, "atoms: absorption must be >= 0");
+      if (f.natoms > 0 && (!f.atom_xyz || !f.atom_species || !f.atom_B || !f.ff_a || !f.ff_b))
+        fail(MB_ERR_ARG, "atoms: arrays missing");
+      for (int a = 0; a < f.natoms; ++a) {
+        const int sp = f.atom_species[a];
+        if (sp < 0 || sp >= f.nspecies) fail(MB_ERR_CONFIG, "atoms: species index out of range");
+        if (!(f.atom_B[a] >= 0.0)) fail(MB_ERR_CONFIG, "atoms: need B >= 0");
+        for (int q = 0; q < 3; ++q)
+          if (!std::isfinite(f.atom_xyz[3 * a + q])) fail(MB_ERR_CONFIG, "atoms: nonfinite position");
+        for (int i = 0; i < 4; ++i)
+          if (!(f.ff_b[4 * sp + i] + f.atom_B[a] > 0.0))
+            fail(MB_ERR_CONFIG, "atoms: form-factor widths b_i + B must be positive");
+      }
+      return;
+    default:
+      fail(MB_ERR_CONFIG, "potential: unknown field kind");
+  }
+}
+
+// Hermite evaluation of a tabulated field at z (potential.cpp:115-148,186-199),
+// host side: the device consumes the resulting node-slot table.
+struct Tabulated {
+  std::vector<double> z;
+  std::vector<std::vector<cd>> y, s;  // [diff][grid]
+};
+Tabulated bind_tabulated(const mb_field& f, const RodTables& rt) {
+  std::map<std::pair<int, int>, int> by_dm;
+  for (int e = 0; e < f.nentries; ++e) by_dm[{f.entry_dm[2 * e], f.entry_dm[2 * e + 1]}] = e;
+  Tabulated t;
+  t.z.assign(f.z_grid, f.z_grid + f.ngrid);
+  const std::size_t g = t.z.size();
+  for (std::size_t d = 0; d < rt.diff.size(); ++d) {
+    auto it = by_dm.find(rt.diff_m[d]);
+    if (it == by_dm.end())
+      fail(MB_ERR_CONFIG, "potential: tabulated field lacks coefficient for rod difference (" +
+                              std::to_string(rt.diff_m[d].first) + "," + std::to_string(rt.diff_m[d].second) + ")");
+    std::vector<cd> y(g), s(g);
+    for (std::size_t i = 0; i < g; ++i)
+      y[i] = cd(f.entry_values[((std::size_t)it->second * g + i) * 2], f.entry_values[((std::size_t)it->second * g + i) * 2 + 1]);
+    const std::vector<double>& z = t.z;
+    if (g == 2) {
+      s[0] = s[1] = (y[1] - y[0]) / (z[1] - z[0]);
+    } else {
+      for (std::size_t i = 1; i + 1 < g; ++i) {
+        const double hl = z[i] - z[i - 1], hr = z[i + 1] - z[i];
+        s[i] = ((y[i + 1] - y[i]) / hr * hl + (y[i] - y[i - 1]) / hl * hr) / (hl + hr);
+      }
+      const double h0 = z[1] - z[0], h1 = z[2] - z[1];
+      s[0] = -(2.0 * h0 + h1) / (h0 * (h0 + h1)) * y[0] + (h0 + h1) / (h0 * h1) * y[1] - h0 / (h1 * (h0 + h1)) * y[2];
+      const double k0 = z[g - 2] - z[g - 3], k1 = z[g - 1] - z[g - 2];
+      s[g - 1] = k1 / (k0 * (k0 + k1)) * y[g - 3] - (k0 + k1) / (k0 * k1) * y[g - 2] +
+                 (2.0 * k1 + k0) / (k1 * (k0 + k1)) * y[g - 1];
+    }
+    t.y.push_back(std::move(y));
+    t.s.push_back(std::move(s));
+  }
+  return t;
+}
+double map_z(double z, double zb) {  // potential.cpp:152-167 without bulk
+  if (z > 1e-9 || !std::isfinite(z)) fail(MB_ERR_DOMAIN, "potential evaluated above the surface");
+  if (z > 0.0) z = 0.0;
+  if (z >= zb) return z;
+  if (z >= zb - 1e-9) return zb;
+  fail(MB_ERR_DOMAIN, "potential evaluated below z_bottom without a bulk period");
+}
+void eval_tabulated(const Tabulated& t, double zb, double z, cd* out) {
+  const double zm = map_z(z, zb);
+  const std::size_t g = t.z.size();
+  std::size_t i = (std::size_t)(std::upper_bound(t.z.begin(), t.z.end(), zm) - t.z.begin());
+  if (i == 0) i = 1;
+  if (i >= g) i = g - 1;
+  const double zl = t.z[i - 1], zr = t.z[i], h = zr - zl;
+  const double tt = std::clamp((zm - zl) / h, 0.0, 1.0);
+  const double t2 = tt * tt, t3 = t2 * tt;
+  const double h00 = 2 * t3 - 3 * t2 + 1, h10 = t3 - 2 * t2 + tt, h01 = -2 * t3 + 3 * t2, h11 = t3 - t2;
+  for (std::size_t d = 0; d < t.y.size(); ++d)
+    out[d] = h00 * t.y[d][i - 1] + h10 * h * t.s[d][i - 1] + h01 * t.y[d][i] + h11 * h * t.s[d][i];
+}
+
+// ------------------------------------------------------------------ context
+struct DevBuf {
+  void* p = nullptr;
+  std::size_t bytes = 0;
+};
+
+}  // namespace
+
+struct mb_context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+};
+
+struct mb_plan {
+  mb_context* ctx = nullptr;
+  int n = 0, ndiff = 0, npad = 0;
+  long npairs = 0, nslots = 0;
+  int S = 0, T = 0;
+  bool use_k1 = false;
+  std::vector<DevBuf> bufs;
+  mbx::PotentialParams pot{};
+  mbx::PropagateParams prop{};
+  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  float ms_total = 0, ms_pot = 0, ms_prop = 0;
+  int launches = 0;
+  bool executed = false;
+  std::vector<double2> host_coef;  // tabulated / zero fields: precomputed table
+};
+
+namespace {
+
+template <class T>
+T* dev_upload(mb_plan* pl, const T* src, std::size_t count) {
+  DevBuf b;
+  b.bytes = std::max<std::size_t>(count * sizeof(T), 16);
+  cuda_check(cudaMallocAsync(&b.p, b.bytes, pl->ctx->stream), "cudaMallocAsync");
+  pl->bufs.push_back(b);
+  if (count && src)
+    cuda_check(cudaMemcpyAsync(b.p, src, count * sizeof(T), cudaMemcpyHostToDevice, pl->ctx->stream), "cudaMemcpyAsync H2D");
+  return static_cast<T*>(b.p);
+}
+template <class T>
+T* dev_alloc(mb_plan* pl, std::size_t count) {
+  return dev_upload<T>(pl, nullptr, count);
+}
+
+void free_plan(mb_plan* pl) {
+  if (!pl) return;
+  if (pl->ctx) {
+    for (DevBuf& b : pl->bufs)
+      if (b.p) cudaFreeAsync(b.p, pl->ctx->stream);
+    cudaStreamSynchronize(pl->ctx->stream);
+  }
+  for (cudaEvent_t& e : pl->ev)
+    if (e) cudaEventDestroy(e);
+  delete pl;
+}
+
+mb_rods rods_view(const RodTables& t, std::vector<double>& k, std::vector<int>& m, std::vector<double>& diff,
+                  std::vector<int>& dm) {
+  for (const Rod& r : t.rods) {
+    k.push_back(r.k.x);
+    k.push_back(r.k.y);
+    m.push_back(r.m1);
+    m.push_back(r.m2);
+  }
+  for (std::size_t d = 0; d < t.diff.size(); ++d) {
+    diff.push_back(t.diff[d].x);
+    diff.push_back(t.diff[d].y);
+    dm.push_back(t.diff_m[d].first);
+    dm.push_back(t.diff_m[d].second);
+  }
+  return mb_rods{(int)t.rods.size(), k.data(), m.data(), (int)t.diff.size(), diff.data(), dm.data(),
+                 t.diff_index.data()};
+}
+
+mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* fields, int nfields, double gamma,
+                     const mb_pair* pairs, long npairs, const mb_stepper* stepper, const mb_options* opts) {
+  if (!ctx || !rods || !fields || !pairs || !stepper || !opts) fail(MB_ERR_ARG, "null argument");
+  if (nfields < 1 || npairs < 1) fail(MB_ERR_ARG, "need at least one field and one pair");
+  const int n = rods->n, ndiff = rods->ndiff;
+  if (n < 1 || ndiff < 1 || !rods->k || !rods->m || !rods->diff || !rods->diff_m || !rods->diff_index)
+    fail(MB_ERR_ARG, "rods: empty or missing arrays");
+  validate_stepper(*stepper);
+  if (!(gamma > 0.0) || !std::isfinite(gamma)) fail(MB_ERR_CONFIG, "beam: gamma must be positive and finite");
+  const double zb = fields[0].z_bottom;
+  for (int f = 0; f < nfields; ++f) {
+    validate_field(fields[f]);
+    if (fields[f].z_bottom != zb) fail(MB_ERR_CONFIG, "batch: every field must share z_bottom");
+    if (fields[f].kind != fields[0].kind) fail(MB_ERR_CONFIG, "batch: every field must be of one kind");
+  }
+  const int npad = mbx::propagate_supported(n, stepper->algorithm == MB_STEP_RK4);
+  if (!npad)
+    fail(MB_ERR_CONFIG, "device path: " + std::to_string(n) + " rods with " +
+                            (stepper->algorithm == MB_STEP_RK4 ? std::string("rk4") : std::string("splitting")) +
+                            " is not covered by a kernel variant yet");
+
+  // slicing (slicing.hpp:17-34) and node heights (stages.cpp:25-30)
+  long L;
+  if (opts->slices > 0) {
+    L = opts->slices;
+  } else {
+    if (!(opts->dz > 0.0) || !std::isfinite(opts->dz)) fail(MB_ERR_CONFIG, "sweep: dz must be positive and finite");
+    L = std::max(1L, std::lround(-zb / opts->dz));
+  }
+  const double h = -zb / (double)L;
+  const Schedule sc = make_schedule(*stepper);
+  const int K = (int)sc.frac.size();
+  const long stride = sc.endpoint_pair() ? K - 1 : K;
+  const long nslots = sc.endpoint_pair() ? L * (K - 1) + 1 : L * K;
+  auto wz = [&](long i) { return (zb * (double)(L - i) + 0.0 * (double)i) / (double)L; };  // StepWindow::z
+  std::vector<double> zslot((std::size_t)nslots);
+  for (long i = 0; i < L; ++i)
+    for (int m = 0; m < K; ++m) {
+      const long slot = i * stride + m;
+      if (slot >= nslots) continue;
+      const double f = sc.frac[m];
+      zslot[(std::size_t)slot] = f == 0.0 ? wz(i) : (f == 1.0 ? wz(i + 1) : wz(i) + f * h);
+    }
+
+  // pairs: AngleGrid semantics per pair, BeamGeometry + GammaMatrix::build
+  // (geometry.cpp:19-57)
+  std::vector<int> pstruct((std::size_t)npairs);
+  std::vector<double> g2((std::size_t)npairs * n), s0((std::size_t)npairs);
+  std::vector<double2> gd((std::size_t)npairs * n), gi((std::size_t)npairs * n);
+  const double gg = gamma * gamma;
+  for (long p = 0; p < npairs; ++p) {
+    const mb_pair& pr = pairs[p];
+    if (pr.structure < 0 || pr.structure >= nfields) fail(MB_ERR_ARG, "pair: structure index out of range");
+    if (!(pr.theta0_deg > 0.0 && pr.theta0_deg < 90.0))
+      fail(MB_ERR_CONFIG, "beam: theta0 must lie in (0, 90) degrees, got " + std::to_string(pr.theta0_deg));
+    if (!std::isfinite(pr.theta1_deg)) fail(MB_ERR_CONFIG, "beam: theta1 must be finite");
+    pstruct[(std::size_t)p] = pr.structure;
+    const double c0 = std::cos(pr.theta0_deg * kDegToRad);
+    const double t1 = pr.theta1_deg * kDegToRad;
+    const double bx = gamma * c0 * std::cos(t1), by = gamma * c0 * std::sin(t1);
+    s0[(std::size_t)p] = std::sin(pr.theta0_deg * kDegToRad);
+    for (int i = 0; i < n; ++i) {
+      const double px = bx + rods->k[2 * i], py = by + rods->k[2 * i + 1];
+      const double d = gg - (px * px + py * py);
+      if (std::abs(d) < 1e-12)
+        fail(MB_ERR_CONFIG, "rod " + std::to_string(i) + " emerges at grazing: |gamma^2 - ||b0+k||^2| = " +
+                                std::to_string(std::abs(d)));
+      const std::size_t o = (std::size_t)p * n + i;
+      g2[o] = d;
+      const cd G = d > 0.0 ? cd(std::sqrt(d), 0.0) : cd(0.0, std::sqrt(-d));
+      const cd Gi = 1.0 / G;
+      gd[o] = make_double2(G.real(), G.imag());
+      gi[o] = make_double2(Gi.real(), Gi.imag());
+    }
+  }
+
+  // lattice box of rod differences: U(j,k) = box[center + off_j - off_k]
+  int M1 = 0, M2 = 0;
+  for (int d = 0; d < ndiff; ++d) {
+    M1 = std::max(M1, std::abs(rods->diff_m[2 * d]));
+    M2 = std::max(M2, std::abs(rods->diff_m[2 * d + 1]));
+  }
+  const int W2 = 2 * M2 + 1, W1 = 2 * M1 + 1;
+  const int box_size = W1 * W2, center = M1 * W2 + M2;
+  std::vector<int> boxpos((std::size_t)ndiff), rowoff((std::size_t)n);
+  for (int d = 0; d < ndiff; ++d) boxpos[(std::size_t)d] = center + rods->diff_m[2 * d] * W2 + rods->diff_m[2 * d + 1];
+  for (int j = 0; j < n; ++j) rowoff[(std::size_t)j] = rods->m[2 * j] * W2 + rods->m[2 * j + 1];
+  for (int j = 0; j < n; ++j)
+    for (int k = 0; k < n; ++k) {
+      const int d = rods->diff_index[(std::size_t)j * n + k];
+      if (d < 0 || d >= ndiff || boxpos[(std::size_t)d] != center + rowoff[(std::size_t)j] - rowoff[(std::size_t)k])
+        fail(MB_ERR_ARG, "rods: diff_index inconsistent with m / diff_m");
+    }
+
+  mb_plan* pl = new mb_plan();
+  pl->ctx = ctx;
+  try {
+    cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    pl->n = n;
+    pl->ndiff = ndiff;
+    pl->npad = npad;
+    pl->npairs = npairs;
+    pl->nslots = nslots;
+    pl->S = nfields;
+    cudaStream_t st = ctx->stream;
+
+    // ---- coefficient table: K1 terms (atoms / gaussian layers) or host table
+    double2* coef = dev_alloc<double2>(pl, (std::size_t)nfields * nslots * ndiff);
+    const int kind = fields[0].kind;
+    if (kind == MB_FIELD_ATOMS || kind == MB_FIELD_GAUSSIAN_LAYERS) {
+      int T = 0;
+      for (int f = 0; f < nfields; ++f)
+        T = std::max(T, kind == MB_FIELD_ATOMS ? 4 * fields[f].natoms : fields[f].nlayers);
+      T = std::max(T, 1);
+      std::vector<double> zc((std::size_t)nfields * T, 0.0), alpha((std::size_t)nfields * T, 0.0),
+          latk((std::size_t)nfields * T, 0.0);
+      std::vector<double2> cpre((std::size_t)nfields * T, make_double2(0.0, 0.0)),
+          xy((std::size_t)nfields * T, make_double2(0.0, 0.0));
+      for (int f = 0; f < nfields; ++f) {
+        const mb_field& F = fields[f];
+        if (kind == MB_FIELD_ATOMS) {
+          // pre = (sign - i*absorption) gamma_L 4 pi / A
+          const cd pre = cd(F.particle_sign, -F.absorption) * (F.gamma_L * 4.0 * kPi / F.cell_area);
+          for (int a = 0; a < F.natoms; ++a)
+            for (int i = 0; i < 4; ++i) {
+              const std::size_t t = (std::size_t)f * T + 4 * a + i;
+              const int sp = F.atom_species[a];
+              const double bp = F.ff_b[4 * sp + i] + F.atom_B[a];
+              const double w = F.ff_a[4 * sp + i] * 2.0 * std::sqrt(kPi) / std::sqrt(bp);
+              const cd c = pre * w;
+              cpre[t] = make_double2(c.real(), c.imag());
+              latk[t] = bp / (16.0 * kPi * kPi);
+              alpha[t] = 4.0 * kPi * kPi / bp;
+              zc[t] = F.atom_xyz[3 * a + 2];
+              xy[t] = make_double2(F.atom_xyz[3 * a], F.atom_xyz[3 * a + 1]);
+            }
+        } else {
+          // GaussianLayer (potential.hpp:11-23): amplitude (1 + i absorption)
+          // * exp(-|dk|^2 / 2 sxy^2) * exp(-(z - zc)^2 / 2 sz^2)
+          for (int l = 0; l < F.nlayers; ++l) {
+            const double* L5 = F.layers + 5 * l;
+            const std::size_t t = (std::size_t)f * T + l;
+            cpre[t] = make_double2(L5[1], L5[1] * L5[4]);
+            latk[t] = 1.0 / (2.0 * L5[2] * L5[2]);
+            alpha[t] = 1.0 / (2.0 * L5[3] * L5[3]);
+            zc[t] = L5[0];
+          }
+        }
+      }
+      std::vector<double2> dg((std::size_t)ndiff);
+      for (int d = 0; d < ndiff; ++d) dg[(std::size_t)d] = make_double2(rods->diff[2 * d], rods->diff[2 * d + 1]);
+      pl->T = T;
+      pl->use_k1 = true;
+      mbx::PotentialParams& pp = pl->pot;
+      pp.S = nfields;
+      pp.T = T;
+      pp.ndiff = ndiff;
+      pp.nslots = nslots;
+      pp.z_slot = dev_upload(pl, zslot.data(), zslot.size());
+      pp.diff_g = dev_upload(pl, dg.data(), dg.size());
+      pp.term_zc = dev_upload(pl, zc.data(), zc.size());
+      pp.term_alpha = dev_upload(pl, alpha.data(), alpha.size());
+      pp.term_latk = dev_upload(pl, latk.data(), latk.size());
+      pp.term_cpre = dev_upload(pl, cpre.data(), cpre.size());
+      pp.term_xy = dev_upload(pl, xy.data(), xy.size());
+      pp.amp = dev_alloc<double2>(pl, (std::size_t)nfields * T * ndiff);
+      pp.coef = coef;
+    } else {
+      // zero or tabulated: node-slot table evaluated on the host once
+      pl->host_coef.assign((std::size_t)nfields * nslots * ndiff, make_double2(0.0, 0.0));
+      if (kind == MB_FIELD_TABULATED) {
+        RodTables rt;
+        for (int d = 0; d < ndiff; ++d) rt.diff_m.push_back({rods->diff_m[2 * d], rods->diff_m[2 * d + 1]});
+        rt.diff.resize((std::size_t)ndiff);
+        std::vector<cd> row((std::size_t)ndiff);
+        for (int f = 0; f < nfields; ++f) {
+          const Tabulated tb = bind_tabulated(fields[f], rt);
+          for (long sl = 0; sl < nslots; ++sl) {
+            eval_tabulated(tb, zb, zslot[(std::size_t)sl], row.data());
+            for (int d = 0; d < ndiff; ++d)
+              pl->host_coef[((std::size_t)f * nslots + sl) * ndiff + d] = make_double2(row[d].real(), row[d].imag());
+          }
+        }
+      }
+      cuda_check(cudaMemcpyAsync(coef, pl->host_coef.data(), pl->host_coef.size() * sizeof(double2),
+                                 cudaMemcpyHostToDevice, st),
+                 "upload coefficient table");
+    }
+
+    // ---- propagation parameters
+    mbx::PropagateParams& p = pl->prop;
+    p.n = n;
+    p.ndiff = ndiff;
+    p.nsteps = (int)L;
+    p.nslots = nslots;
+    p.npairs = npairs;
+    p.coef = coef;
+    p.boxpos = dev_upload(pl, boxpos.data(), boxpos.size());
+    p.rowoff = dev_upload(pl, rowoff.data(), rowoff.size());
+    p.box_size = box_size;
+    p.box_center = center;
+    p.pair_struct = dev_upload(pl, pstruct.data(), pstruct.size());
+    p.gamma2 = dev_upload(pl, g2.data(), g2.size());
+    p.gdiag = dev_upload(pl, gd.data(), gd.size());
+    p.ginv = dev_upload(pl, gi.data(), gi.size());
+    p.sin_theta0 = dev_upload(pl, s0.data(), s0.size());
+    p.rk4 = stepper->algorithm == MB_STEP_RK4;
+    p.variant = stepper->variant;
+    p.slot_stride = (int)stride;
+    p.h = h;
+    if (p.rk4) {
+      p.nocc = 4;
+      for (int r = 0; r < 4; ++r) p.occ_node[r] = sc.occ2node[(std::size_t)r];
+    } else {
+      p.nocc = stepper->nkick;
+      for (int r = 0; r < stepper->nkick; ++r) {
+        p.occ_node[r] = sc.occ2node[(std::size_t)r];
+        p.occ_kick[r] = h * stepper->kick[r];
+      }
+      for (int r = 0; r < stepper->ndrift; ++r) p.occ_drift[r] = h * stepper->drift[r];
+      p.final_drift = stepper->variant == MB_SPLIT_ABA ? h * stepper->drift[stepper->ndrift - 1] : 0.0;
+      const bool can_fsal = stepper->variant == MB_SPLIT_BAB && sc.endpoint_pair() &&
+                            sc.occ2node.front() == 0 && sc.occ2node.back() == K - 1;
+      p.fsal = (opts->fsal && can_fsal) ? 1 : 0;
+      p.fsal_kick = h * (stepper->kick[stepper->nkick - 1] + stepper->kick[0]);
+    }
+    p.threshold = opts->rhst_threshold;
+    p.residual_check = opts->residual_check ? 1 : 0;
+    p.eta = dev_alloc<double>(pl, (std::size_t)npairs * n);
+    p.rho = dev_alloc<double2>(pl, (std::size_t)npairs * n);
+    p.status = dev_alloc<mbx::PointStatus>(pl, (std::size_t)npairs);
+    for (cudaEvent_t& e : pl->ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+  } catch (...) {
+    free_plan(pl);
+    throw;
+  }
+  return pl;
+}
+
+void execute_plan(mb_plan* pl, cudaStream_t st) {
+  cuda_check(cudaSetDevice(pl->ctx->device), "cudaSetDevice");
+  if (!st) st = pl->ctx->stream;
+  pl->launches = 0;
+  cuda_check(cudaEventRecord(pl->ev[0], st), "event");
+  if (pl->use_k1) cuda_check(mbx::launch_potential(pl->pot, st, &pl->launches), "potential kernel launch");
+  cuda_check(cudaEventRecord(pl->ev[1], st), "event");
+  int npad = 0;
+  cuda_check(mbx::launch_propagate(pl->prop, st, &pl->launches, &npad), "propagation kernel launch");
+  cuda_check(cudaEventRecord(pl->ev[2], st), "event");
+  cuda_check(cudaEventSynchronize(pl->ev[2]), "propagation kernel");
+  cuda_check(cudaGetLastError(), "kernel execution");
+  cudaEventElapsedTime(&pl->ms_pot, pl->ev[0], pl->ev[1]);
+  cudaEventElapsedTime(&pl->ms_prop, pl->ev[1], pl->ev[2]);
+  cudaEventElapsedTime(&pl->ms_total, pl->ev[0], pl->ev[2]);
+  pl->executed = true;
+}
+
+int collect_results(mb_plan* pl, double* eta, double* rho, mb_point_status* status) {
+  if (!pl->executed) fail(MB_ERR_ARG, "plan has not been executed");
+  cudaStream_t st = pl->ctx->stream;
+  const std::size_t ne = (std::size_t)pl->npairs * pl->n;
+  std::vector<mbx::PointStatus> stv((std::size_t)pl->npairs);
+  if (eta) cuda_check(cudaMemcpyAsync(eta, pl->prop.eta, ne * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H eta");
+  if (rho) cuda_check(cudaMemcpyAsync(rho, pl->prop.rho, ne * sizeof(double2), cudaMemcpyDeviceToHost, st), "D2H rho");
+  cuda_check(cudaMemcpyAsync(stv.data(), pl->prop.status, stv.size() * sizeof(mbx::PointStatus),
+                             cudaMemcpyDeviceToHost, st),
+             "D2H status");
+  cuda_check(cudaStreamSynchronize(st), "D2H");
+  if (status)
+    for (std::size_t i = 0; i < stv.size(); ++i)
+      status[i] = mb_point_status{stv[i].code, stv[i].step, stv[i].rhst, 0};
+  for (std::size_t i = 0; i < stv.size(); ++i) {
+    if (stv[i].code == MB_POINT_OK) continue;
+    const std::string where = " (pair " + std::to_string(i) + ", step " + std::to_string(stv[i].step) + ")";
+    if (stv[i].code == MB_POINT_NONFINITE) fail(MB_ERR_BREAKDOWN, "propagation state went nonfinite" + where);
+    if (stv[i].code == MB_POINT_RHST)
+      fail(MB_ERR_BREAKDOWN, "stabilizing transform: solve_right: singular or ill-conditioned system" + where);
+    fail(MB_ERR_BREAKDOWN, "reflection extraction: solve_right: singular or ill-conditioned system" + where);
+  }
+  return MB_OK;
+}
+
+}  // namespace
+
+// ====================================================================== C-ABI
+extern "C" {
+
+const char* mb_last_error(void) { return g_last_error.c_str(); }
+
+int mb_device_ok(int device) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || device < 0 || device >= count) return 0;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return 0;
+  return prop.major == 10 && prop.minor == 0;
+}
+
+int mb_rods_build(const mb_lattice* lattice, double cutoff, int first_n, int* n, int* ndiff, double* k, int* m,
+                  double* diff, int* diff_m, int* diff_index, int cap_n, int cap_diff) {
+  return guarded([&] {
+    if (!lattice || !n || !ndiff) fail(MB_ERR_ARG, "null argument");
+    const Lattice lat{V2{lattice->a1[0], lattice->a1[1]}, V2{lattice->a2[0], lattice->a2[1]}};
+    const RodTables t = build_rods(lat, cutoff, first_n);
+    const int nn = (int)t.rods.size(), nd = (int)t.diff.size();
+    *n = nn;
+    *ndiff = nd;
+    if (!k && !m && !diff && !diff_m && !diff_index) return;
+    if (cap_n < nn || cap_diff < nd) fail(MB_ERR_ARG, "mb_rods_build: capacity too small");
+    for (int i = 0; i < nn; ++i) {
+      if (k) {
+        k[2 * i] = t.rods[i].k.x;
+        k[2 * i + 1] = t.rods[i].k.y;
+      }
+      if (m) {
+        m[2 * i] = t.rods[i].m1;
+        m[2 * i + 1] = t.rods[i].m2;
+      }
+    }
+    for (int d = 0; d < nd; ++d) {
+      if (diff) {
+        diff[2 * d] = t.diff[d].x;
+        diff[2 * d + 1] = t.diff[d].y;
+      }
+      if (diff_m) {
+        diff_m[2 * d] = t.diff_m[d].first;
+        diff_m[2 * d + 1] = t.diff_m[d].second;
+      }
+    }
+    if (diff_index) std::memcpy(diff_index, t.diff_index.data(), t.diff_index.size() * sizeof(int));
+  });
+}
+
+int mb_beam_from_energy(double e, double* gamma, double* gamma_L) {
+  return guarded([&] {
+    if (!gamma || !gamma_L) fail(MB_ERR_ARG, "null argument");
+    if (!(e > 0.0) || !std::isfinite(e)) fail(MB_ERR_CONFIG, "beam: energy must be positive");
+    const double mc2 = 510998.95, hc = 12398.419843320026;
+    const double lambda = hc / std::sqrt(e * (e + 2.0 * mc2));
+    *gamma = kTwoPi / lambda;
+    *gamma_L = 1.0 + e / mc2;
+  });
+}
+
+int mb_stepper_by_name(const char* name, mb_stepper* out) {
+  return guarded([&] {
+    if (!name || !out) fail(MB_ERR_ARG, "null argument");
+    const std::string s(name);
+    const Tables& t = tables();
+    if (s == "rk4") {
+      *out = mb_stepper{MB_STEP_RK4, MB_SPLIT_BAB, 0, nullptr, 0, nullptr};
+    } else if (s == "sp4") {
+      *out = mb_stepper{MB_STEP_SPLITTING, MB_SPLIT_BAB, 6, t.sp4_drift, 7, t.sp4_kick};
+    } else if (s == "sp6") {
+      *out = mb_stepper{MB_STEP_SPLITTING, MB_SPLIT_BAB, 11, t.sp6_drift, 12, t.sp6_kick};
+    } else {
+      fail(MB_ERR_CONFIG, "unknown stepper '" + s + "' (expected rk4, sp4 or sp6)");
+    }
+  });
+}
+
+int mb_context_create(int device, mb_context** out) {
+  return guarded([&] {
+    if (!out) fail(MB_ERR_ARG, "null argument");
+    *out = nullptr;
+    int count = 0;
+    cuda_check(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
+    if (device < 0 || device >= count) fail(MB_ERR_CUDA, "no such CUDA device");
+    if (!mb_device_ok(device)) fail(MB_ERR_CUDA, "device is not an sm_100 (B200) GPU; no CPU fallback exists");
+    cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    auto* ctx = new mb_context();
+    ctx->device = device;
+    cudaError_t e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+      delete ctx;
+      cuda_check(e, "cudaStreamCreate");
+    }
+    // keep freed plan memory in the pool for the next call
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    *out = ctx;
+  });
+}
+
+int mb_context_destroy(mb_context* ctx) {
+  return guarded([&] {
+    if (!ctx) return;
+    cudaStreamSynchronize(ctx->stream);
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+  });
+}
+
+int mb_plan_create(mb_context* ctx, const mb_rods* rods, const mb_field* fields, int nfields, double gamma,
+                   const mb_pair* pairs, long npairs, const mb_stepper* stepper, const mb_options* opts,
+                   mb_plan** out) {
+  return guarded([&] {
+    if (!out || !ctx) fail(MB_ERR_ARG, "null argument");
+    *out = nullptr;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    *out = create_plan(ctx, rods, fields, nfields, gamma, pairs, npairs, stepper, opts);
+    cuda_check(cudaStreamSynchronize(ctx->stream), "plan upload");
+  });
+}
+
+int mb_plan_execute(mb_plan* plan, void* stream) {
+  return guarded([&] {
+    if (!plan) fail(MB_ERR_ARG, "null plan");
+    std::lock_guard<std::mutex> lk(plan->ctx->mu);
+    execute_plan(plan, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int mb_plan_results(mb_plan* plan, double* eta, double* rho, mb_point_status* status) {
+  int rc = MB_OK;
+  const int g = guarded([&] {
+    if (!plan) fail(MB_ERR_ARG, "null plan");
+    std::lock_guard<std::mutex> lk(plan->ctx->mu);
+    rc = collect_results(plan, eta, rho, status);
+  });
+  return g != MB_OK ? g : rc;
+}
+
+int mb_plan_timing(const mb_plan* plan, double* ms_total, double* ms_potential, double* ms_propagate, int* launches) {
+  return guarded([&] {
+    if (!plan) fail(MB_ERR_ARG, "null plan");
+    if (ms_total) *ms_total = plan->ms_total;
+    if (ms_potential) *ms_potential = plan->ms_pot;
+    if (ms_propagate) *ms_propagate = plan->ms_prop;
+    if (launches) *launches = plan->launches;
+  });
+}
+
+int mb_plan_info(const mb_plan* plan, long* slots, int* ndiff, long* coef_bytes, int* npad) {
+  return guarded([&] {
+    if (!plan) fail(MB_ERR_ARG, "null plan");
+    if (slots) *slots = plan->nslots;
+    if (ndiff) *ndiff = plan->ndiff;
+    if (coef_bytes) *coef_bytes = (long)plan->S * plan->nslots * plan->ndiff * (long)sizeof(double2);
+    if (npad) *npad = plan->npad;
+  });
+}
+
+int mb_plan_destroy(mb_plan* plan) {
+  return guarded([&] {
+    if (!plan) return;
+    std::lock_guard<std::mutex> lk(plan->ctx->mu);
+    free_plan(plan);
+  });
+}
+
+int mb_rocking_curve(mb_context* ctx, const mb_field* field, const mb_rods* rods, double gamma, const double* theta0,
+                     int n_theta0, const double* theta1, int n_theta1, const mb_stepper* stepper,
+                     const mb_options* opts, double* eta, double* rho, mb_point_status* status) {
+  mb_plan* plan = nullptr;
+  int rc = guarded([&] {
+    if (!theta0 || !theta1 || !eta) fail(MB_ERR_ARG, "null argument");
+    // AngleGrid::validated (sweep.cpp:18-33)
+    if (n_theta0 < 1) fail(MB_ERR_CONFIG, "angle grid: theta0 list is empty");
+    if (n_theta1 < 1) fail(MB_ERR_CONFIG, "angle grid: theta1 list is empty");
+    for (int i = 0; i < n_theta0; ++i)
+      if (!(theta0[i] > 0.0 && theta0[i] < 90.0))
+        fail(MB_ERR_CONFIG, "angle grid: glancing angles must lie in (0, 90) degrees");
+    for (int i = 1; i < n_theta0; ++i)
+      if (!(theta0[i] > theta0[i - 1])) fail(MB_ERR_CONFIG, "angle grid: theta0 must be strictly increasing");
+    for (int i = 0; i < n_theta1; ++i)
+      if (!std::isfinite(theta1[i])) fail(MB_ERR_CONFIG, "angle grid: theta1 must be finite");
+    std::vector<mb_pair> pairs;
+    for (int b = 0; b < n_theta1; ++b)
+      for (int a = 0; a < n_theta0; ++a) pairs.push_back(mb_pair{0, theta0[a], theta1[b]});
+    if (!ctx) fail(MB_ERR_ARG, "null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    plan = create_plan(ctx, rods, field, 1, gamma, pairs.data(), (long)pairs.size(), stepper, opts);
+    execute_plan(plan, nullptr);
+  });
+  if (rc != MB_OK) {
+    if (plan) mb_plan_destroy(plan);
+    return rc;
+  }
+  rc = mb_plan_results(plan, eta, rho, status);
+  const std::string err = g_last_error;
+  mb_plan_destroy(plan);
+  g_last_error = err;
+  return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,80 @@
+// Internal structures shared by the host runtime (mb_host.cpp) and the sm_100a
+// kernels (mb_kernels.cu). Not part of the public ABI.
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace mbx {
+
+constexpr int kMaxOcc = 32;  // kick occurrences (or RK stages) per step
+
+// Point status on the device (mirrors mb_point_status)
+struct PointStatus {
+  int code, step, rhst, reserved;
+};
+
+// ---- K1: slice-potential coefficients --------------------------------------
+// coef[s][slot][d] = sum_t amp[s][t][d] * exp(-alpha[s][t] * (z[slot] - zc[s][t])^2)
+// amp[s][t][d]     = cpre[s][t] * lat * e^{-i g_d . rho_t}   (atoms)
+//                  = cpre[s][t] * lat                         (gaussian layers)
+// lat              = exp(-lat_k[s][t] * |g_d|^2)
+struct PotentialParams {
+  int S, T, ndiff;
+  long nslots;
+  const double* z_slot;   // [nslots]
+  const double2* diff_g;  // [ndiff] (gx, gy), 1/A
+  const double* term_zc;  // [S*T]
+  const double* term_alpha;
+  const double* term_latk;
+  const double2* term_cpre;  // complex prefactor
+  const double2* term_xy;    // in-plane position (atoms) or (0,0)
+  double2* amp;              // [S][T][ndiff] scratch
+  double2* coef;             // [S][nslots][ndiff]
+};
+
+// ---- K2: propagation + RHST + extraction + intensity -----------------------
+struct PropagateParams {
+  int n, ndiff;
+  int nsteps;
+  long nslots;
+  long npairs;
+  // coefficient table and its box scatter
+  const double2* coef;     // [S][nslots][ndiff]
+  const int* boxpos;       // [ndiff] -> position inside the smem box table
+  const int* rowoff;       // [n] -> m1*W2 + m2 (box row offset of rod j)
+  int box_size, box_center;
+  // pairs
+  const int* pair_struct;     // [npairs]
+  const double* gamma2;       // [npairs][n]  Gamma^2 (real)
+  const double2* gdiag;       // [npairs][n]  Gamma
+  const double2* ginv;        // [npairs][n]  1/Gamma
+  const double* sin_theta0;   // [npairs]
+  // stepper
+  int rk4;                    // 1 = classical RK4
+  int variant;                // splitting: 0 ABA, 1 BAB
+  int nocc;                   // table occurrences per step (RK4: 4 stages)
+  int slot_stride;            // slots per step
+  int occ_node[kMaxOcc];      // node index within the step per occurrence
+  double occ_kick[kMaxOcc];   // h * b_r per kick occurrence (splitting)
+  double occ_drift[kMaxOcc];  // h * a_r (BAB: after kick r; ABA: before kick r)
+  double final_drift;         // ABA: trailing drift h * a_s
+  double fsal_kick;           // BAB + fsal: merged coefficient h*(b_s + b_0)
+  int fsal;
+  double h;
+  double threshold;
+  int residual_check;
+  // outputs
+  double* eta;                // [npairs][n]
+  double2* rho;               // [npairs][n]
+  PointStatus* status;        // [npairs]
+};
+
+// launchers (mb_kernels.cu)
+cudaError_t launch_potential(const PotentialParams& p, cudaStream_t st, int* launches);
+// returns cudaErrorInvalidValue when no kernel variant covers n / stepper
+cudaError_t launch_propagate(const PropagateParams& p, cudaStream_t st, int* launches, int* npad);
+int propagate_supported(int n, int rk4);  // padded size or 0
+
+}  // namespace mbx

@@ -1,0 +1,904 @@
+// sm_100a kernels of the B200-native forward model.
+//
+//   K1  potential_amp_kernel / potential_coef_kernel
+//       slice-potential coefficients u(dg, z_slot) for every node slot of the
+//       slicing plan (replaces BoundPotential::eval_coeffs + UTable,
+//       /root/reference/proj/core/src/potential.cpp:169-207, stages.cpp:32-47).
+//   K2  propagate_kernel<Cfg, RK4>
+//       one CTA per (structure, angle) pair; the economical state [Q; P]
+//       stays on chip for all slices (proposed.cpp:275-289). Per kick / RK
+//       stage the complex product U*X runs on the FP64 tensor pipe
+//       (mma.sync m8n8k4 f64 -> DMMA.8x8x4) with U gathered on the fly from the
+//       node's compact coefficient table staged in shared memory (cp.async),
+//       so no N x N U matrix ever touches HBM. Fused: Gershgorin estimate and
+//       RHST (kernels.cpp:82-99, proposed.cpp:196-202) as an in-CTA
+//       Gauss-Jordan column elimination with partial pivoting plus the 1e-10
+//       residual gate of solve_right (kernels.cpp:60-80); the surface solve
+//       R T^-1 (proposed.cpp:204-208) with the same machinery; intensity
+//       (curve.cpp:8-20).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "mb_internal.h"
+
+namespace mbx {
+
+// ============================================================== helpers
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+__device__ __forceinline__ double dneg(double x) {
+  return __longlong_as_double(__double_as_longlong(x) ^ (long long)0x8000000000000000ULL);
+}
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// complex helpers on (re, im) pairs
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cinv(double2 a) {  // 1/a with scaling (Smith)
+  if (fabs(a.x) >= fabs(a.y)) {
+    const double r = a.y / a.x, d = a.x + a.y * r;
+    return make_double2(1.0 / d, -r / d);
+  }
+  const double r = a.x / a.y, d = a.y + a.x * r;
+  return make_double2(r / d, -1.0 / d);
+}
+
+// ============================================================== K1
+// amp[s][t][d] = cpre * exp(-latk |g|^2) * exp(-i g.xy)
+__global__ void potential_amp_kernel(const __grid_constant__ PotentialParams p) {
+  const long total = (long)p.S * p.T * p.ndiff;
+  for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long)gridDim.x * blockDim.x) {
+    const int d = (int)(idx % p.ndiff);
+    const long st = idx / p.ndiff;  // s*T + t
+    const double2 g = p.diff_g[d];
+    const double lat = exp(-p.term_latk[st] * (g.x * g.x + g.y * g.y));
+    const double2 xy = p.term_xy[st];
+    const double ph = -(g.x * xy.x + g.y * xy.y);
+    double sn, cs;
+    sincos(ph, &sn, &cs);
+    const double2 c = p.term_cpre[st];
+    const double2 cl = make_double2(c.x * lat, c.y * lat);
+    p.amp[idx] = cmul(cl, make_double2(cs, sn));
+  }
+}
+
+// coef[s][slot][d] = sum_t amp[s][t][d] * exp(-alpha_t (z_slot - zc_t)^2)
+// grid: (slot blocks of kSlotTile, S); threads over d. The z-Gaussians of the
+// slot tile are staged in shared memory; every amp element is read once per
+// tile and reused kSlotTile times from registers.
+constexpr int kSlotTile = 16;
+__global__ void __launch_bounds__(128) potential_coef_kernel(const __grid_constant__ PotentialParams p) {
+  extern __shared__ double zg[];  // [T][kSlotTile]
+  const int s = blockIdx.y;
+  const long slot0 = (long)blockIdx.x * kSlotTile;
+  const int nsl = (int)min((long)kSlotTile, p.nslots - slot0);
+  for (int i = threadIdx.x; i < p.T * kSlotTile; i += blockDim.x) {
+    const int t = i / kSlotTile, q = i % kSlotTile;
+    double v = 0.0;
+    if (q < nsl) {
+      const double dz = p.z_slot[slot0 + q] - p.term_zc[(long)s * p.T + t];
+      v = exp(-p.term_alpha[(long)s * p.T + t] * dz * dz);
+    }
+    zg[i] = v;
+  }
+  __syncthreads();
+  const double2* amp = p.amp + (long)s * p.T * p.ndiff;
+  for (int d = threadIdx.x; d < p.ndiff; d += blockDim.x) {
+    double re[kSlotTile], im[kSlotTile];
+#pragma unroll
+    for (int q = 0; q < kSlotTile; ++q) re[q] = im[q] = 0.0;
+    for (int t = 0; t < p.T; ++t) {
+      const double2 a = amp[(long)t * p.ndiff + d];
+#pragma unroll
+      for (int q = 0; q < kSlotTile; ++q) {
+        const double g = zg[t * kSlotTile + q];
+        re[q] = fma(a.x, g, re[q]);
+        im[q] = fma(a.y, g, im[q]);
+      }
+    }
+    double2* out = p.coef + ((long)s * p.nslots + slot0) * p.ndiff + d;
+#pragma unroll
+    for (int q = 0; q < kSlotTile; ++q)
+      if (q < nsl) out[(long)q * p.ndiff] = make_double2(re[q], im[q]);
+  }
+}
+
+cudaError_t launch_potential(const PotentialParams& p, cudaStream_t st, int* launches) {
+  const long total = (long)p.S * p.T * p.ndiff;
+  if (total > 0) {
+    const int blocks = (int)min((total + 255) / 256, (long)148 * 16);
+    potential_amp_kernel<<<blocks, 256, 0, st>>>(p);
+    ++*launches;
+  }
+  dim3 grid((unsigned)((p.nslots + kSlotTile - 1) / kSlotTile), (unsigned)p.S);
+  const size_t smem = (size_t)p.T * kSlotTile * sizeof(double);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(potential_coef_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  potential_coef_kernel<<<grid, 128, smem, st>>>(p);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+// ============================================================== K2
+// Tile configuration: NP = padded rod count; WM x WN warps; each warp owns a
+// (NP/WM) x (NP/WN) complex tile = MB x NB blocks of 8x8 (DMMA C fragments).
+template <int NP_, int WM_, int WN_>
+struct Cfg {
+  static constexpr int NP = NP_, WM = WM_, WN = WN_;
+  static constexpr int NW = WM * WN, NT = NW * 32;
+  static constexpr int TM = NP / WM, TN = NP / WN;
+  static constexpr int MB = TM / 8, NB = TN / 8;
+  static_assert(TM % 8 == 0 && TN % 8 == 0, "tile must be a multiple of 8");
+};
+
+// swizzled row-major plane: element (r, c) of an NP x NP matrix. The XOR keeps
+// DMMA B-fragment loads (4 rows x 8 cols per warp) and dense A-fragment loads
+// (8 rows x 4 cols) free of bank conflicts without padding.
+template <int NP>
+__device__ __forceinline__ int sw(int r, int c) {
+  return r * NP + (c ^ ((r & 3) << 2));
+}
+
+// own-element accessors: v[mb][nb][0..3] = re(r,c), re(r,c+1), im(r,c), im(r,c+1)
+template <class C>
+struct Own {
+  int row0, col0, lane;
+  __device__ __forceinline__ int r(int mb) const { return row0 + mb * 8 + (lane >> 2); }
+  __device__ __forceinline__ int c(int nb) const { return col0 + nb * 8 + 2 * (lane & 3); }
+  __device__ __forceinline__ void ld(const double* Xr, const double* Xi, int mb, int nb, double (&v)[4]) const {
+    const int o = sw<C::NP>(r(mb), c(nb));
+    const double2 a = *reinterpret_cast<const double2*>(Xr + o);
+    const double2 b = *reinterpret_cast<const double2*>(Xi + o);
+    v[0] = a.x;
+    v[1] = a.y;
+    v[2] = b.x;
+    v[3] = b.y;
+  }
+  __device__ __forceinline__ void st(double* Xr, double* Xi, int mb, int nb, const double (&v)[4]) const {
+    const int o = sw<C::NP>(r(mb), c(nb));
+    *reinterpret_cast<double2*>(Xr + o) = make_double2(v[0], v[1]);
+    *reinterpret_cast<double2*>(Xi + o) = make_double2(v[2], v[3]);
+  }
+  __device__ __forceinline__ void load(const double* Xr, const double* Xi, double (&v)[C::MB][C::NB][4]) const {
+#pragma unroll
+    for (int mb = 0; mb < C::MB; ++mb)
+#pragma unroll
+      for (int nb = 0; nb < C::NB; ++nb) {
+        const int o = sw<C::NP>(r(mb), c(nb));
+        const double2 a = *reinterpret_cast<const double2*>(Xr + o);
+        const double2 b = *reinterpret_cast<const double2*>(Xi + o);
+        v[mb][nb][0] = a.x;
+        v[mb][nb][1] = a.y;
+        v[mb][nb][2] = b.x;
+        v[mb][nb][3] = b.y;
+      }
+  }
+  __device__ __forceinline__ void store(double* Xr, double* Xi, const double (&v)[C::MB][C::NB][4]) const {
+#pragma unroll
+    for (int mb = 0; mb < C::MB; ++mb)
+#pragma unroll
+      for (int nb = 0; nb < C::NB; ++nb) {
+        const int o = sw<C::NP>(r(mb), c(nb));
+        *reinterpret_cast<double2*>(Xr + o) = make_double2(v[mb][nb][0], v[mb][nb][1]);
+        *reinterpret_cast<double2*>(Xi + o) = make_double2(v[mb][nb][2], v[mb][nb][3]);
+      }
+  }
+};
+
+template <class C>
+__device__ __forceinline__ void zero(double (&v)[C::MB][C::NB][4]) {
+#pragma unroll
+  for (int mb = 0; mb < C::MB; ++mb)
+#pragma unroll
+    for (int nb = 0; nb < C::NB; ++nb)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[mb][nb][q] = 0.0;
+}
+
+// acc = U * X, U gathered from the node's box table: U(j,k) = box[raddr_j - off_k]
+// (raddr_j = center + off_j, or -1 for padded rows -> 0). X rows k >= n are zero
+// by construction, so padded columns of U need no mask.
+template <class C>
+__device__ __forceinline__ void gemm_box(double (&acc)[C::MB][C::NB][4], const double2* __restrict__ box,
+                                         const int* __restrict__ soff, const int (&raddr)[C::MB],
+                                         const double* __restrict__ Xr, const double* __restrict__ Xi,
+                                         int col0, int lane, int kmax) {
+  zero<C>(acc);
+  const int kl = lane & 3, cl = lane >> 2;
+#pragma unroll 2
+  for (int k0 = 0; k0 < kmax; k0 += 4) {
+    const int k = k0 + kl;
+    const int offk = soff[k];
+    double ar[C::MB], ai[C::MB], an[C::MB];
+#pragma unroll
+    for (int mb = 0; mb < C::MB; ++mb) {
+      double2 a = make_double2(0.0, 0.0);
+      if (raddr[mb] >= 0) a = box[raddr[mb] - offk];
+      ar[mb] = a.x;
+      ai[mb] = a.y;
+      an[mb] = dneg(a.y);
+    }
+    double br[C::NB], bi[C::NB];
+#pragma unroll
+    for (int nb = 0; nb < C::NB; ++nb) {
+      const int o = sw<C::NP>(k, col0 + nb * 8 + cl);
+      br[nb] = Xr[o];
+      bi[nb] = Xi[o];
+    }
+#pragma unroll
+    for (int mb = 0; mb < C::MB; ++mb)
+#pragma unroll
+      for (int nb = 0; nb < C::NB; ++nb) {
+        dmma(acc[mb][nb][0], acc[mb][nb][1], ar[mb], br[nb]);
+        dmma(acc[mb][nb][0], acc[mb][nb][1], an[mb], bi[nb]);
+        dmma(acc[mb][nb][2], acc[mb][nb][3], ar[mb], bi[nb]);
+        dmma(acc[mb][nb][2], acc[mb][nb][3], ai[mb], br[nb]);
+      }
+  }
+}
+
+// acc = A * X with a dense A in shared memory (residual gate of solve_right)
+template <class C>
+__device__ __forceinline__ void gemm_dense(double (&acc)[C::MB][C::NB][4], const double* __restrict__ Ar,
+                                           const double* __restrict__ Ai, const double* __restrict__ Xr,
+                                           const double* __restrict__ Xi, int row0, int col0, int lane,
+                                           int kmax) {
+  zero<C>(acc);
+  const int kl = lane & 3, cl = lane >> 2;
+  for (int k0 = 0; k0 < kmax; k0 += 4) {
+    const int k = k0 + kl;
+    double ar[C::MB], ai[C::MB], an[C::MB];
+#pragma unroll
+    for (int mb = 0; mb < C::MB; ++mb) {
+      const int o = sw<C::NP>(row0 + mb * 8 + cl, k);
+      ar[mb] = Ar[o];
+      ai[mb] = Ai[o];
+      an[mb] = dneg(ai[mb]);
+    }
+    double br[C::NB], bi[C::NB];
+#pragma unroll
+    for (int nb = 0; nb < C::NB; ++nb) {
+      const int o = sw<C::NP>(k, col0 + nb * 8 + cl);
+      br[nb] = Xr[o];
+      bi[nb] = Xi[o];
+    }
+#pragma unroll
+    for (int mb = 0; mb < C::MB; ++mb)
+#pragma unroll
+      for (int nb = 0; nb < C::NB; ++nb) {
+        dmma(acc[mb][nb][0], acc[mb][nb][1], ar[mb], br[nb]);
+        dmma(acc[mb][nb][0], acc[mb][nb][1], an[mb], bi[nb]);
+        dmma(acc[mb][nb][2], acc[mb][nb][3], ar[mb], bi[nb]);
+        dmma(acc[mb][nb][2], acc[mb][nb][3], ai[mb], br[nb]);
+      }
+  }
+}
+
+// shared scratch for the block-level reductions / Gauss-Jordan
+struct Scratch {
+  double red_a[32], red_b[32];
+  int red_i[32];
+  int piv;
+  double pivval;
+  double2 inv;
+};
+
+// Gershgorin condition estimate of the n x n block of Q (kernels.cpp:82-99):
+// max_i(|q_ii| + r_i) / min_i(|q_ii| - r_i), +inf if any |q_ii| - r_i <= 0.
+template <class C>
+__device__ double gershgorin(const double* Qr, const double* Qi, int n, Scratch& sc, int warp, int lane) {
+  double hi = 0.0, lo = __longlong_as_double(0x7ff0000000000000LL);
+  int bad = 0;
+  for (int i = warp; i < n; i += C::NW) {
+    double rs = 0.0, dg = 0.0;
+    for (int j = lane; j < n; j += 32) {
+      const int o = sw<C::NP>(i, j);
+      const double a = hypot(Qr[o], Qi[o]);
+      if (j == i)
+        dg = a;
+      else
+        rs += a;
+    }
+    rs = warp_sum(rs);
+    dg = warp_sum(dg);
+    hi = fmax(hi, dg + rs);
+    if (dg - rs <= 0.0) bad = 1;
+    lo = fmin(lo, dg - rs);
+  }
+  if (lane == 0) {
+    sc.red_a[warp] = hi;
+    sc.red_b[warp] = lo;
+    sc.red_i[warp] = bad;
+  }
+  __syncthreads();
+  double H = 0.0, L = __longlong_as_double(0x7ff0000000000000LL);
+  int B = 0;
+#pragma unroll
+  for (int w = 0; w < C::NW; ++w) {
+    H = fmax(H, sc.red_a[w]);
+    L = fmin(L, sc.red_b[w]);
+    B |= sc.red_i[w];
+  }
+  __syncthreads();  // scratch reusable
+  if (n == 0) return 1.0;
+  if (B) return __longlong_as_double(0x7ff0000000000000LL);
+  return H / L;
+}
+
+// B <- B * A^-1 for the n x n blocks (A destroyed): Gauss-Jordan column
+// elimination with partial pivoting on row k of A (== Eigen PartialPivLU of
+// A^T pivoting on column k, first maximum wins; kernels.cpp:66-71).
+// Returns false on an exactly zero pivot (kernels.cpp:68-71).
+template <class C>
+__device__ bool gauss_jordan(double* Ar, double* Ai, double* Br, double* Bi, double2* fv, int n, Scratch& sc,
+                             int tid, int warp, int lane) {
+  for (int k = 0; k < n; ++k) {
+    if (warp == 0) {
+      double best = -1.0;
+      int bj = n;
+      for (int j = k + lane; j < n; j += 32) {
+        const int o = sw<C::NP>(k, j);
+        const double v = hypot(Ar[o], Ai[o]);
+        if (v > best) {
+          best = v;
+          bj = j;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+        if (ob > best || (ob == best && oj < bj)) {
+          best = ob;
+          bj = oj;
+        }
+      }
+      const int p = bj;
+      // multipliers of the post-swap row k: f_j = A[k][j] (j != k)
+      for (int j = lane; j < n; j += 32) {
+        double2 f = make_double2(0.0, 0.0);
+        if (j != k) {
+          const int src = (j == p) ? k : j;
+          const int o = sw<C::NP>(k, src);
+          f = make_double2(Ar[o], Ai[o]);
+        }
+        fv[j] = f;
+      }
+      if (lane == 0) {
+        sc.piv = p;
+        sc.pivval = best;
+        const int o = sw<C::NP>(k, p);
+        sc.inv = best > 0.0 ? cinv(make_double2(Ar[o], Ai[o])) : make_double2(0.0, 0.0);
+      }
+    }
+    __syncthreads();
+    if (!(sc.pivval > 0.0)) return false;
+    const int p = sc.piv;
+    const double2 inv = sc.inv;
+    for (int i = tid; i < n; i += C::NT) {
+      const int ok = sw<C::NP>(i, k), op = sw<C::NP>(i, p);
+      double2 a = make_double2(Ar[op], Ai[op]);
+      double2 b = make_double2(Br[op], Bi[op]);
+      if (p != k) {
+        Ar[op] = Ar[ok];
+        Ai[op] = Ai[ok];
+        Br[op] = Br[ok];
+        Bi[op] = Bi[ok];
+      }
+      a = cmul(a, inv);
+      b = cmul(b, inv);
+      Ar[ok] = a.x;
+      Ai[ok] = a.y;
+      Br[ok] = b.x;
+      Bi[ok] = b.y;
+    }
+    __syncthreads();
+    // eliminate: col_j -= f_j col_k for j != k. A rows < k are final (unit) and
+    // never read again; B needs every row.
+    const int rowsA = n - k;
+    const int work = (rowsA + n) * n;
+    for (int w = tid; w < work; w += C::NT) {
+      const int i2 = w / n, j = w % n;
+      if (j == k) continue;
+      const double2 f = fv[j];
+      if (i2 < rowsA) {
+        const int i = k + i2;
+        const double2 x = make_double2(Ar[sw<C::NP>(i, k)], Ai[sw<C::NP>(i, k)]);
+        const int o = sw<C::NP>(i, j);
+        Ar[o] -= f.x * x.x - f.y * x.y;
+        Ai[o] -= f.x * x.y + f.y * x.x;
+      } else {
+        const int i = i2 - rowsA;
+        const double2 x = make_double2(Br[sw<C::NP>(i, k)], Bi[sw<C::NP>(i, k)]);
+        const int o = sw<C::NP>(i, j);
+        Br[o] -= f.x * x.x - f.y * x.y;
+        Bi[o] -= f.x * x.y + f.y * x.x;
+      }
+    }
+    __syncthreads();
+  }
+  return true;
+}
+
+// identity on the n x n block, zero elsewhere
+template <class C>
+__device__ void set_identity(double* Xr, double* Xi, int n, int tid) {
+  for (int w = tid; w < C::NP * C::NP; w += C::NT) {
+    const int r = w / C::NP, c = w % C::NP;
+    Xr[sw<C::NP>(r, c)] = (r == c && r < n) ? 1.0 : 0.0;
+    Xi[sw<C::NP>(r, c)] = 0.0;
+  }
+}
+
+// solve_right residual gate (kernels.cpp:73-79): ||X A0 - B0||_F / ||B0||_F <= 1e-10.
+// X dense in (Xr, Xi); A0 own elements in a0 (written into (Ar, Ai) first);
+// B0 own elements in b0.
+template <class C>
+__device__ bool residual_ok(double* Ar, double* Ai, const double* Xr, const double* Xi,
+                            const double (&a0)[C::MB][C::NB][4], const double (&b0)[C::MB][C::NB][4],
+                            double (&acc)[C::MB][C::NB][4], const Own<C>& own, int n, Scratch& sc, int warp,
+                            int lane) {
+  own.store(Ar, Ai, a0);
+  __syncthreads();
+  gemm_dense<C>(acc, Xr, Xi, Ar, Ai, own.row0, own.col0, lane, (n + 3) & ~3);
+  double rn = 0.0, bn = 0.0, bad = 0.0;
+#pragma unroll
+  for (int mb = 0; mb < C::MB; ++mb)
+#pragma unroll
+    for (int nb = 0; nb < C::NB; ++nb)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double d = acc[mb][nb][q] - b0[mb][nb][q];
+        rn += d * d;
+        bn += b0[mb][nb][q] * b0[mb][nb][q];
+        if (!isfinite(acc[mb][nb][q])) bad = 1.0;
+      }
+  rn = warp_sum(rn);
+  bn = warp_sum(bn);
+  bad = warp_sum(bad);
+  if (lane == 0) {
+    sc.red_a[warp] = rn;
+    sc.red_b[warp] = bn;
+    sc.red_i[warp] = bad > 0.0;
+  }
+  __syncthreads();
+  double R = 0.0, Bn = 0.0;
+  int B = 0;
+#pragma unroll
+  for (int w = 0; w < C::NW; ++w) {
+    R += sc.red_a[w];
+    Bn += sc.red_b[w];
+    B |= sc.red_i[w];
+  }
+  __syncthreads();
+  const double bnorm = sqrt(Bn);
+  const double resid = sqrt(R) / (bnorm > 0.0 ? bnorm : 1.0);
+  return (resid <= 1e-10) && !B;
+}
+
+template <class C, bool RK4>
+__global__ void __launch_bounds__(C::NT, 1) propagate_kernel(const __grid_constant__ PropagateParams p) {
+  constexpr int NP = C::NP, MB = C::MB, NB = C::NB;
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* Ar = reinterpret_cast<double*>(smem);
+  double* Ai = Ar + NP * NP;
+  double* Br = Ai + NP * NP;
+  double* Bi = Br + NP * NP;
+  double* Cr = Bi + NP * NP;  // RK4 only
+  double* Ci = Cr + NP * NP;
+  double2* box0 = reinterpret_cast<double2*>(RK4 ? Ci + NP * NP : Cr);
+  double2* box1 = box0 + p.box_size;
+  double2* fv = box1 + p.box_size;           // [NP]
+  double* g2s = reinterpret_cast<double*>(fv + NP);  // [NP]
+  int* soff = reinterpret_cast<int*>(g2s + NP);      // [NP]
+  Scratch* sc = reinterpret_cast<Scratch*>(soff + NP);
+  int* sboxpos = reinterpret_cast<int*>(sc + 1);     // [ndiff]
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n = p.n;
+  const long pair = blockIdx.x;
+  const int wm = warp / C::WN, wn = warp % C::WN;
+  Own<C> own{wm * C::TM, wn * C::TN, lane};
+  const double2* coef = p.coef + (long)p.pair_struct[pair] * p.nslots * p.ndiff;
+  const int kmax = (n + 3) & ~3;
+
+  for (int i = tid; i < p.ndiff; i += C::NT) sboxpos[i] = p.boxpos[i];
+  for (int i = tid; i < NP; i += C::NT) {
+    soff[i] = i < n ? p.rowoff[i] : 0;
+    g2s[i] = i < n ? p.gamma2[pair * n + i] : 0.0;
+  }
+  // initial_state (proposed.cpp:123-128) with R_init = 0:
+  // Q = diag(ginv)/2, P = (i/2) I on the n x n block, zero padding.
+  for (int w = tid; w < NP * NP; w += C::NT) {
+    Ar[w] = 0.0;
+    Ai[w] = 0.0;
+  }
+  __syncthreads();
+  for (int i = tid; i < n; i += C::NT) {
+    const double2 gi = p.ginv[pair * n + i];
+    Ar[sw<NP>(i, i)] = 0.5 * gi.x;
+    Ai[sw<NP>(i, i)] = 0.5 * gi.y;
+  }
+  double P[MB][NB][4];
+#pragma unroll
+  for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int r = own.r(mb), c = own.c(nb) + e;
+        P[mb][nb][e] = 0.0;
+        P[mb][nb][2 + e] = (r == c && r < n) ? 0.5 : 0.0;
+      }
+  int raddr[MB];
+#pragma unroll
+  for (int mb = 0; mb < MB; ++mb) {
+    const int r = own.r(mb);
+    raddr[mb] = r < n ? p.box_center + p.rowoff[r] : -1;
+  }
+
+  double acc[MB][NB][4];
+  double SQ[RK4 ? MB : 1][RK4 ? NB : 1][4];
+  double SAVE[MB][NB][4];
+
+  // table pipeline: occurrence o = step * nocc + r; slot = step*stride + node
+  auto slot_of = [&](int step, int r) -> long { return (long)step * p.slot_stride + p.occ_node[r]; };
+  auto issue = [&](double2* dst, long slot) {
+    const double2* src = coef + slot * p.ndiff;
+    for (int d = tid; d < p.ndiff; d += C::NT) cp_async16(dst + sboxpos[d], src + d);
+    cp_async_commit();
+  };
+  double2* cur = box0;
+  double2* nxt = box1;
+  __syncthreads();  // sboxpos ready
+  const int r_first = 0;
+  long cur_slot = slot_of(0, r_first);
+  issue(cur, cur_slot);
+
+  int rhst = 0;
+  int code = 0, fail_step = 0;
+  const int nocc = p.nocc;
+  const int L = p.nsteps;
+  const bool fsal = !RK4 && p.fsal && p.variant == 1;
+
+  // advance the table pipeline to occurrence (step, r); returns the box to use
+  auto begin_occ = [&](int step, int r, int nstep, int nr) -> double2* {
+    cp_async_wait_all();
+    __syncthreads();
+    if (nstep < L) {
+      const long ns = slot_of(nstep, nr);
+      if (ns != cur_slot) {
+        issue(nxt, ns);
+        double2* b = cur;
+        // current box stays `cur` for this occurrence; swap after use
+        (void)b;
+      }
+    }
+    return cur;
+  };
+  auto end_occ = [&](int nstep, int nr) {
+    if (nstep < L) {
+      const long ns = slot_of(nstep, nr);
+      if (ns != cur_slot) {
+        double2* t = cur;
+        cur = nxt;
+        nxt = t;
+        cur_slot = ns;
+      }
+    }
+  };
+
+#define FOR_BLK _Pragma("unroll") for (int mb = 0; mb < MB; ++mb) _Pragma("unroll") for (int nb = 0; nb < NB; ++nb)
+  // Q += c * P on own elements (caller orders the other warps' reads of A)
+  auto drift = [&](double c) {
+    FOR_BLK {
+      double q0[4];
+      own.ld(Ar, Ai, mb, nb, q0);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) q0[q] += c * P[mb][nb][q];
+      own.st(Ar, Ai, mb, nb, q0);
+    }
+  };
+  for (int step = 0; step < L; ++step) {
+    if constexpr (RK4) {
+      // ---------------- classical RK4 (proposed.cpp:141-168), restructured:
+      // Qnew = Q + hP + h^2/6 (K1+K2+K3), Pnew = P + h/6 (K1 + 2K2 + 2K3 + K4),
+      // X2 = Q + h/2 P, X3 = X2 + h^2/4 K1, X4 = Q + hP + h^2/2 K2, K = -(U+G^2) X
+      const double h = p.h;
+      FOR_BLK {  // B = X2 = Q + h/2 P
+        double v[4];
+        own.ld(Ar, Ai, mb, nb, v);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[q] += (0.5 * h) * P[mb][nb][q];
+        own.st(Br, Bi, mb, nb, v);
+      }
+      // stage 1 (foot) on Q (A)
+      double2* box = begin_occ(step, 0, step, 1);
+      gemm_box<C>(acc, box, soff, raddr, Ar, Ai, own.col0, lane, kmax);
+      end_occ(step, 1);
+      FOR_BLK {
+        double q0[4], x2[4];
+        own.ld(Ar, Ai, mb, nb, q0);
+        own.ld(Br, Bi, mb, nb, x2);
+        const double g2 = g2s[own.r(mb)];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double K = -(acc[mb][nb][q] + g2 * q0[q]);
+          acc[mb][nb][q] = K;
+          SQ[mb][nb][q] = K;
+          x2[q] += (0.25 * h * h) * K;  // X3
+        }
+        own.st(Cr, Ci, mb, nb, x2);
+      }
+      __syncthreads();  // every warp finished reading A in the stage-1 GEMM
+      FOR_BLK {
+        double q0[4];
+        own.ld(Ar, Ai, mb, nb, q0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          q0[q] += h * P[mb][nb][q];  // Qbase = Q + hP
+          P[mb][nb][q] += (h / 6.0) * acc[mb][nb][q];
+        }
+        own.st(Ar, Ai, mb, nb, q0);
+      }
+      // stage 2 (mid) on X2 (B)
+      box = begin_occ(step, 1, step, 2);
+      gemm_box<C>(acc, box, soff, raddr, Br, Bi, own.col0, lane, kmax);
+      end_occ(step, 2);
+      FOR_BLK {
+        double x2[4];
+        own.ld(Br, Bi, mb, nb, x2);
+        const double g2 = g2s[own.r(mb)];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double K = -(acc[mb][nb][q] + g2 * x2[q]);
+          acc[mb][nb][q] = K;
+          SQ[mb][nb][q] += K;
+          P[mb][nb][q] += (h / 3.0) * K;
+        }
+      }
+      __syncthreads();  // every warp finished reading B
+      FOR_BLK {  // B = X4 = Qbase + h^2/2 K2
+        double qb[4];
+        own.ld(Ar, Ai, mb, nb, qb);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) qb[q] += (0.5 * h * h) * acc[mb][nb][q];
+        own.st(Br, Bi, mb, nb, qb);
+      }
+      // stage 3 (mid) on X3 (C)
+      box = begin_occ(step, 2, step, 3);
+      gemm_box<C>(acc, box, soff, raddr, Cr, Ci, own.col0, lane, kmax);
+      end_occ(step, 3);
+      FOR_BLK {
+        double x3[4];
+        own.ld(Cr, Ci, mb, nb, x3);
+        const double g2 = g2s[own.r(mb)];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double K = -(acc[mb][nb][q] + g2 * x3[q]);
+          SQ[mb][nb][q] += K;
+          P[mb][nb][q] += (h / 3.0) * K;
+        }
+      }
+      // stage 4 (top) on X4 (B)
+      box = begin_occ(step, 3, step + 1, 0);
+      gemm_box<C>(acc, box, soff, raddr, Br, Bi, own.col0, lane, kmax);
+      end_occ(step + 1, 0);
+      FOR_BLK {
+        double x4[4], qb[4];
+        own.ld(Br, Bi, mb, nb, x4);
+        own.ld(Ar, Ai, mb, nb, qb);
+        const double g2 = g2s[own.r(mb)];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double K = -(acc[mb][nb][q] + g2 * x4[q]);
+          P[mb][nb][q] += (h / 6.0) * K;
+          qb[q] += (h * h / 6.0) * SQ[mb][nb][q];
+        }
+        own.st(Ar, Ai, mb, nb, qb);
+      }
+    } else {
+      // ---------------- splitting (proposed.cpp:170-194)
+      // BAB: nocc = s+1 kicks, drifts after kicks 0..s-1; ABA: nocc = s kicks,
+      // a drift before every kick plus a trailing drift.
+      int r0 = 0;
+      if (fsal && step > 0) {
+        // kick 0 of this step was merged into the previous step's last kick
+        // (same node height); its drift still runs. The end-of-step barrier
+        // already ordered every read of A.
+        drift(p.occ_drift[0]);
+        r0 = 1;
+      }
+      for (int r = r0; r < nocc; ++r) {
+        const bool last = (r == nocc - 1);
+        const int nstep = last ? step + 1 : step;
+        const int nr = last ? ((fsal && step + 1 > 0) ? 1 : 0) : r + 1;
+        if (p.variant == 0) {  // ABA: drift before kick r
+          __syncthreads();  // previous kick's GEMM reads of A complete
+          drift(p.occ_drift[r]);
+        }
+        double2* box = begin_occ(step, r, nstep, nr);
+        gemm_box<C>(acc, box, soff, raddr, Ar, Ai, own.col0, lane, kmax);
+        end_occ(nstep, nr);
+        const double kc = (fsal && last && step + 1 < L) ? p.fsal_kick : p.occ_kick[r];
+        FOR_BLK {
+          double q0[4];
+          own.ld(Ar, Ai, mb, nb, q0);
+          const double g2 = g2s[own.r(mb)];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) P[mb][nb][q] -= kc * (acc[mb][nb][q] + g2 * q0[q]);
+        }
+        if (p.variant == 1 && !last) {  // BAB: drift after kick r
+          __syncthreads();  // all warps done reading A
+          drift(p.occ_drift[r]);
+        }
+      }
+      if (p.variant == 0) {  // ABA trailing drift
+        __syncthreads();
+        drift(p.final_drift);
+      }
+    }
+
+    // ---------------- end of step: finite check, Gershgorin, RHST
+    // (proposed.cpp:279-287)
+    {
+      int bad = 0;
+      FOR_BLK {
+        double q0[4];
+        own.ld(Ar, Ai, mb, nb, q0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) bad |= !isfinite(P[mb][nb][q]) || !isfinite(q0[q]);
+      }
+      if (__syncthreads_or(bad)) {
+        code = 1;
+        fail_step = step;
+        break;
+      }
+    }
+    const double xi = gershgorin<C>(Ar, Ai, n, *sc, warp, lane);
+    if (xi > p.threshold) {
+      // P <- P Q^-1, Q <- I. B is free scratch here for both steppers.
+      double (&Q0)[MB][NB][4] = SAVE;  // Q kept for the residual gate
+      if (p.residual_check) own.load(Ar, Ai, Q0);
+      own.store(Br, Bi, P);
+      __syncthreads();
+      bool ok = gauss_jordan<C>(Ar, Ai, Br, Bi, fv, n, *sc, tid, warp, lane);
+      if (ok && p.residual_check) ok = residual_ok<C>(Ar, Ai, Br, Bi, Q0, P, acc, own, n, *sc, warp, lane);
+      if (!ok) {
+        code = 2;
+        fail_step = step;
+        break;
+      }
+      own.load(Br, Bi, P);
+      __syncthreads();
+      set_identity<C>(Ar, Ai, n, tid);
+      ++rhst;
+    }
+    __syncthreads();
+  }
+  cp_async_wait_all();
+  __syncthreads();
+
+  // ---------------- surface solve: X = R T^-1 (proposed.cpp:204-208), rho = X[:,0]
+  if (code == 0) {
+    double T0[MB][NB][4], Rr[MB][NB][4];
+    {
+      double Q0[MB][NB][4];
+      own.load(Ar, Ai, Q0);
+#pragma unroll
+      for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb) {
+          const int r = own.r(mb);
+          const double2 g = r < n ? p.gdiag[pair * n + r] : make_double2(0.0, 0.0);
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const double qr = Q0[mb][nb][e], qi = Q0[mb][nb][2 + e];
+            const double gqr = g.x * qr - g.y * qi, gqi = g.x * qi + g.y * qr;
+            const double pr = P[mb][nb][e], pi = P[mb][nb][2 + e];
+            // T = G Q - i P, R = G Q + i P   (i*P = (-pi, pr))
+            T0[mb][nb][e] = gqr + pi;
+            T0[mb][nb][2 + e] = gqi - pr;
+            Rr[mb][nb][e] = gqr - pi;
+            Rr[mb][nb][2 + e] = gqi + pr;
+          }
+        }
+    }
+    __syncthreads();
+    own.store(Ar, Ai, T0);
+    own.store(Br, Bi, Rr);
+    __syncthreads();
+    bool ok = gauss_jordan<C>(Ar, Ai, Br, Bi, fv, n, *sc, tid, warp, lane);
+    if (ok && p.residual_check) ok = residual_ok<C>(Ar, Ai, Br, Bi, T0, Rr, acc, own, n, *sc, warp, lane);
+    if (!ok) {
+      code = 3;
+      fail_step = L;
+    } else {
+      // intensity (curve.cpp:8-20)
+      const double s0 = p.sin_theta0[pair];
+      const double g0 = p.gdiag[pair * n].x;
+      for (int i = tid; i < n; i += C::NT) {
+        const int o = sw<NP>(i, 0);
+        const double2 rho = make_double2(Br[o], Bi[o]);
+        const double2 gi = p.gdiag[pair * n + i];
+        const bool prop = gi.y == 0.0;  // geometry.cpp:46-50: propagating rods have real Gamma
+        p.rho[pair * n + i] = rho;
+        p.eta[pair * n + i] = prop ? (rho.x * rho.x + rho.y * rho.y) * s0 * g0 / gi.x : 0.0;
+      }
+    }
+  }
+  if (tid == 0) {
+    PointStatus st;
+    st.code = code;
+    st.step = fail_step;
+    st.rhst = rhst;
+    st.reserved = 0;
+    p.status[pair] = st;
+  }
+}
+
+// ============================================================== dispatch
+template <class C, bool RK4>
+static size_t smem_bytes(const PropagateParams& p) {
+  const int np = C::NP;
+  size_t b = (size_t)(RK4 ? 6 : 4) * np * np * sizeof(double);
+  b += 2 * (size_t)p.box_size * sizeof(double2);
+  b += (size_t)np * sizeof(double2) + (size_t)np * sizeof(double) + (size_t)np * sizeof(int);
+  b += sizeof(Scratch) + 16;
+  b += (size_t)p.ndiff * sizeof(int);
+  return b;
+}
+
+template <class C, bool RK4>
+static cudaError_t launch_cfg(const PropagateParams& p, cudaStream_t st) {
+  const size_t smem = smem_bytes<C, RK4>(p);
+  cudaError_t e = cudaFuncSetAttribute(propagate_kernel<C, RK4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  propagate_kernel<C, RK4><<<(unsigned)p.npairs, C::NT, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+using C16 = Cfg<16, 1, 2>;
+using C32 = Cfg<32, 2, 2>;
+using C64 = Cfg<64, 4, 2>;
+
+int propagate_supported(int n, int rk4) {
+  if (n <= 16) return 16;
+  if (n <= 32) return 32;
+  if (n <= 64) return rk4 ? 0 : 64;
+  return 0;
+}
+
+cudaError_t launch_propagate(const PropagateParams& p, cudaStream_t st, int* launches, int* npad) {
+  const int np = propagate_supported(p.n, p.rk4);
+  *npad = np;
+  cudaError_t e = cudaErrorInvalidValue;
+  if (np == 16) e = p.rk4 ? launch_cfg<C16, true>(p, st) : launch_cfg<C16, false>(p, st);
+  if (np == 32) e = p.rk4 ? launch_cfg<C32, true>(p, st) : launch_cfg<C32, false>(p, st);
+  if (np == 64) e = launch_cfg<C64, false>(p, st);
+  if (e == cudaSuccess) ++*launches;
+  return e;
+}
+
+}  // namespace mbx

@@ -1,0 +1,59 @@
+"""Shared parity harness: runs one workload through the oracle (CPU
+restatement, test infrastructure) and through the device path
+(libmanybeam_b200.so via the Python mirror) on identical seeded inputs."""
+import math
+
+import numpy as np
+
+import paper_2306_00271_b200 as mb
+from paper_2306_00271_b200 import configs
+
+
+def oracle_lattice(o, w):
+    return o.Lattice2D(tuple(w.a1), tuple(w.a2))
+
+
+def oracle_fields(o, w):
+    ff_a, ff_b = configs.form_factors()
+    return [o.PotentialField.atoms(w.z_bottom, s.xyz, s.species.astype(np.int32), s.B, ff_a, ff_b, w.cell_area,
+                                   w.gamma_L, w.sign, w.absorption) for s in w.structures]
+
+
+def run_oracle(o, w, threads=0, method=None, slices=None, threshold=1000.0):
+    """Returns eta [pairs][n], rho, rhst counts; pairs ordered structure-major,
+    theta0 inner (one oracle rocking_curve per structure, as the reference
+    has no batched API)."""
+    rods = o.RodSet.build_first(oracle_lattice(o, w), w.n_rods)
+    opts = o.SweepOptions()
+    opts.method = method or w.method
+    opts.slices = slices or w.slices
+    opts.threads = threads
+    opts.rhst_threshold = threshold
+    grid = o.AngleGrid.validated(list(w.theta0), list(w.theta1))
+    etas, rhos, rh = [], [], []
+    for f in oracle_fields(o, w):
+        c = o.rocking_curve(f, rods, w.gamma, grid, opts)
+        etas.append(c.eta)
+        rhos.append(c.rho)
+        rh.append(c.rhst)
+    return np.concatenate(etas), np.concatenate(rhos), np.concatenate(rh)
+
+
+def run_device(w, method=None, slices=None, threshold=1000.0, residual_check=True, fsal=False):
+    rods = mb.RodSet.build_first(mb.Lattice2D(w.a1, w.a2), w.n_rods)
+    opts = mb.SweepOptions(method=method or w.method, slices=slices or w.slices, rhst_threshold=threshold,
+                           residual_check=residual_check, fsal=fsal)
+    pairs = [(s, t0, t1) for s in range(len(w.structures)) for t1 in w.theta1 for t0 in w.theta0]
+    return mb.solve_batch(configs.product_fields(w), rods, w.gamma, pairs, opts)
+
+
+def curve_err(eta, ref):
+    num = np.linalg.norm(eta - ref, axis=1).max()
+    den = np.linalg.norm(ref, axis=1).max()
+    return 0.0 if num == 0 else (math.inf if den == 0 else num / den)
+
+
+def entry_rel_err(eta, ref):
+    """per-entry relative error on entries above 1e-12 * max eta."""
+    mask = np.abs(ref) > 1e-12 * np.abs(ref).max()
+    return float((np.abs(eta - ref)[mask] / np.abs(ref)[mask]).max())

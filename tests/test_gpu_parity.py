@@ -1,0 +1,196 @@
+"""GPU parity: the device path (C-ABI -> sm_100a kernels) against the oracle
+on identical seeded inputs, plus the reference's own known-answer tests run
+through the device path. Tolerance (BASELINE.json north_star):
+curve_error <= 1e-9 and per-entry relative error <= 1e-9 on entries above
+1e-12 * max eta, complex128 throughout."""
+import math
+
+import numpy as np
+import pytest
+
+import fields as F
+import harness as H
+import paper_2306_00271_b200 as mb
+from paper_2306_00271_b200 import configs
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-9
+
+
+def dev_layered_field():
+    return mb.PotentialField.gaussian_layers(-10.0, F.LAYERED_LAYERS)
+
+
+def dev_rods11():
+    return mb.RodSet.build(mb.Lattice2D(*F.RECT), 5.0)
+
+
+def dev_rods1():
+    return mb.RodSet.build(mb.Lattice2D(*F.RECT), 0.5)
+
+
+def oracle_curve(o, field, rods, gamma, t0, method, dz, threshold=1000.0, threads=4):
+    opts = o.SweepOptions()
+    opts.method, opts.dz, opts.threads, opts.rhst_threshold = method, dz, threads, threshold
+    return o.rocking_curve(field, rods, gamma, o.AngleGrid.validated(t0, [0.0]), opts)
+
+
+@pytest.mark.parametrize("method", ["rk4", "sp4", "sp6"])
+@pytest.mark.parametrize("fsal", [False, True])
+def test_layered_field_parity(oracle, method, fsal):
+    t0 = [2.0, 5.0, 9.0, 12.0, 17.0, 25.0]
+    ref = oracle_curve(oracle, F.layered_field(oracle), F.rods11(oracle), F.K_GAMMA11, t0, method, 0.02)
+    c = mb.rocking_curve(dev_layered_field(), dev_rods11(), F.K_GAMMA11, mb.AngleGrid.validated(t0, [0.0]),
+                         mb.SweepOptions(method=method, dz=0.02, fsal=fsal))
+    assert H.curve_err(c.eta, ref.eta) <= TOL
+    assert H.entry_rel_err(c.eta, ref.eta) <= TOL
+    assert np.abs(c.rho - ref.rho).max() <= 1e-10 * np.abs(ref.rho).max()
+
+
+def test_deep_field_rhst_parity(oracle):  # test_proposed.cpp:211-238 domain
+    t0 = [3.0, 5.0, 7.0]
+    ref = oracle_curve(oracle, F.deep_field(oracle), F.rods11(oracle), F.K_GAMMA11, t0, "sp6", 0.02)
+    field = mb.PotentialField.gaussian_layers(-50.0, F.DEEP_LAYERS)
+    c = mb.rocking_curve(field, dev_rods11(), F.K_GAMMA11, mb.AngleGrid.validated(t0, [0.0]),
+                         mb.SweepOptions(method="sp6", dz=0.02))
+    assert (c.status["rhst"] > 0).all()
+    assert np.array_equal(c.status["rhst"], ref.rhst)
+    assert H.curve_err(c.eta, ref.eta) <= TOL
+
+
+@pytest.mark.parametrize("threshold", [0.0, 1000.0, math.inf])
+def test_threshold_invariance(oracle, threshold):  # test_proposed.cpp:189-209
+    field = mb.PotentialField.gaussian_layers(-2.0, [(-1.0, -0.35, 1.8, 0.4, 0.1)])
+    grid = mb.AngleGrid.validated([12.0, 20.0], [0.0])
+    c = mb.rocking_curve(field, dev_rods11(), F.K_GAMMA11, grid,
+                         mb.SweepOptions(method="sp6", dz=0.005, rhst_threshold=threshold))
+    base = mb.rocking_curve(field, dev_rods11(), F.K_GAMMA11, grid, mb.SweepOptions(method="sp6", dz=0.005))
+    assert np.linalg.norm(c.rho - base.rho) <= 1e-10 * np.linalg.norm(base.rho)
+    if threshold == 0.0:
+        assert (c.status["rhst"] == 400).all()
+    if math.isinf(threshold):
+        assert (c.status["rhst"] == 0).all()
+
+
+def test_fresnel_slab_closed_form():  # test_proposed.cpp:140-158
+    gamma, theta0, z_e, u0 = 2.0, 30.0, -7.0, complex(-0.8, -0.2)
+    g = gamma * math.sin(math.radians(theta0))
+    exp = F.fresnel_slab_rho0(g, u0, z_e)
+    field = mb.PotentialField.tabulated(z_e, [z_e, 0.0], [((0, 0), [u0, u0])])
+    grid = mb.AngleGrid.validated([theta0], [0.0])
+    for method, tol in (("sp6", 1e-6), ("sp4", 1e-4), ("rk4", 1e-4)):
+        c = mb.rocking_curve(field, dev_rods1(), gamma, grid, mb.SweepOptions(method=method, dz=0.01))
+        assert abs(c.rho[0, 0] - exp) <= tol * abs(exp)
+
+
+def test_empirical_order_sp6():  # test_proposed.cpp:160-187 (sp6 ladder)
+    gamma, theta0, z_e, u0 = 2.0, 30.0, -7.0, complex(-0.9, -0.25)
+    g = gamma * math.sin(math.radians(theta0))
+    exp = F.fresnel_slab_rho0(g, u0, z_e)
+    field = mb.PotentialField.tabulated(z_e, [z_e, 0.0], [((0, 0), [u0, u0])])
+    grid = mb.AngleGrid.validated([theta0], [0.0])
+    hs, errs = [], []
+    for n in (6, 8, 10, 14, 20, 28, 40):
+        c = mb.rocking_curve(field, dev_rods1(), gamma, grid, mb.SweepOptions(method="sp6", slices=n))
+        hs.append(-z_e / n)
+        errs.append(abs(c.rho[0, 0] - exp) / abs(exp))
+    assert F.fit_order(hs, errs, 1e-13, 1e-2, 4) == pytest.approx(6.0, rel=0.12)
+
+
+def test_zero_potential():  # acceptance.cpp:69-94
+    field = mb.PotentialField.zero(-1.0)
+    grid = mb.AngleGrid.validated([float(t) for t in range(1, 70)], [0.0])
+    for m in ("rk4", "sp4", "sp6"):
+        c = mb.rocking_curve(field, dev_rods1(), 1.0, grid, mb.SweepOptions(method=m, dz=5e-4))
+        assert np.abs(c.rho).max() <= 1e-12 and np.abs(c.eta).max() <= 1e-24
+
+
+def test_breakdown_surfaces_with_step(oracle):  # test_sweep.cpp:90-105
+    layers = [(-1.0 - 2.0 * i, -0.22, 2.2, 0.7, 0.08) for i in range(75)]
+    field = mb.PotentialField.gaussian_layers(-150.0, layers)
+    grid = mb.AngleGrid.validated([3.0, 5.0], [0.0])
+    with pytest.raises(mb.BreakdownError) as ei:
+        mb.rocking_curve(field, dev_rods11(), F.K_GAMMA11, grid,
+                         mb.SweepOptions(method="sp6", dz=0.02, rhst_threshold=math.inf))
+    assert ei.value.step is not None and 0 < ei.value.step < 7500
+    with pytest.raises(oracle.BreakdownError) as eo:
+        oracle.rocking_curve(F.deep_field(oracle) if False else oracle.PotentialField.gaussian_layers(-150.0, layers),
+                             F.rods11(oracle), F.K_GAMMA11, oracle.AngleGrid.validated([3.0], [0.0]),
+                             _opts(oracle, "sp6", 0.02, math.inf))
+    assert ei.value.step == eo.value.step
+
+
+def _opts(o, method, dz, thr):
+    s = o.SweepOptions()
+    s.method, s.dz, s.rhst_threshold = method, dz, thr
+    return s
+
+
+def test_flux_bound():  # acceptance.cpp:308-319
+    grid = mb.AngleGrid.validated([float(t) for t in range(1, 70)], [0.0])
+    c = mb.rocking_curve(dev_layered_field(), dev_rods11(), F.K_GAMMA11, grid, mb.SweepOptions(method="sp4", dz=0.02))
+    assert c.eta.sum(axis=1).max() <= 1.0 + 1e-8
+
+
+def test_custom_aba_stepper_parity(oracle):
+    # a symmetric ABA splitting (Strang-type 2-stage) through both paths
+    drift, kick = [0.25, 0.5, 0.25], [0.5, 0.5]
+    t0 = [4.0, 11.0]
+    o_spec = oracle.StepperSpec.splitting("aba2", oracle.SplitVariant.ABA, drift, kick)
+    u = oracle.BoundPotential(F.layered_field(oracle), F.rods11(oracle))
+    refs = []
+    for t in t0:
+        gm = F.scalar_gamma(oracle, F.K_GAMMA11, t, F.rods11(oracle))
+        r, _ = oracle.solve_proposed(u, gm, oracle.SlicingPlan.with_target_dz(-10.0, 0.02), o_spec)
+        refs.append(r)
+    spec = mb.StepperSpec.splitting("aba2", mb.StepperSpec.ABA, drift, kick)
+    c = mb.rocking_curve(dev_layered_field(), dev_rods11(), F.K_GAMMA11, mb.AngleGrid.validated(t0, [0.0]),
+                         mb.SweepOptions(dz=0.02, stepper=spec))
+    assert np.abs(c.rho - np.array(refs)).max() <= 1e-10 * np.abs(np.array(refs)).max()
+
+
+def test_deterministic_bitwise():
+    grid = mb.AngleGrid.validated([2.0, 5.0, 8.0, 11.0], [0.0])
+    args = (dev_layered_field(), dev_rods11(), F.K_GAMMA11, grid, mb.SweepOptions(method="sp4", dz=0.02))
+    a, b = mb.rocking_curve(*args), mb.rocking_curve(*args)
+    assert np.array_equal(a.eta, b.eta)
+    # a row solved alone equals the same row inside a batch (fixed per-pair arithmetic)
+    one = mb.rocking_curve(dev_layered_field(), dev_rods11(), F.K_GAMMA11, mb.AngleGrid.validated([8.0], [0.0]),
+                           mb.SweepOptions(method="sp4", dz=0.02))
+    assert np.array_equal(one.eta[0], a.eta[2])
+
+
+# ---------------------------------------------------------------- atom configs
+def test_config0_full_parity(oracle):
+    w = configs.config0()
+    ref, rref, rh = H.run_oracle(oracle, w)
+    eta, rho, st = H.run_device(w)
+    assert H.curve_err(eta, ref) <= TOL
+    assert H.entry_rel_err(eta, ref) <= TOL
+    assert (st["code"] == 0).all()
+
+
+def test_config1_subset_parity(oracle):
+    w = configs.config1().subset(theta0=[0.1, 1.0, 2.5, 6.1])
+    ref, rref, rh = H.run_oracle(oracle, w, threads=4)
+    for fsal in (False, True):
+        eta, rho, st = H.run_device(w, fsal=fsal)
+        assert H.curve_err(eta, ref) <= TOL, fsal
+        assert H.entry_rel_err(eta, ref) <= TOL, fsal
+
+
+def test_config2_subset_parity(oracle):
+    w = configs.config2(n_structures=3).subset(theta0=[0.5, 2.0, 4.4, 6.5])
+    ref, _, _ = H.run_oracle(oracle, w, threads=4)
+    eta, _, st = H.run_device(w)
+    assert H.curve_err(eta, ref) <= TOL
+    assert H.entry_rel_err(eta, ref) <= TOL
+
+
+@pytest.mark.parametrize("n,method", [(15, "rk4"), (15, "sp6"), (31, "sp6"), (63, "sp6")])
+def test_config4_subset_parity(oracle, n, method):
+    w = configs.config4(n, method, n_structures=2).subset(theta0=[0.5, 3.3, 6.8], slices=100)
+    ref, _, _ = H.run_oracle(oracle, w, threads=4)
+    eta, _, st = H.run_device(w)
+    assert H.curve_err(eta, ref) <= TOL
+    assert H.entry_rel_err(eta, ref) <= TOL
