@@ -1,0 +1,292 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native forward model (driver contract).
+
+Default workload: BASELINE.json configs[1] (RHEED, rect 7.68x3.84 A, N=61
+beams, 15 keV electrons, 600 slices, sp6 = the reference's highest-order
+stepper, 121 glancing angles) on synthetic seeded atoms (no dataset exists).
+A "step" is one full pass over the workload: K1 (slice-potential
+coefficients) + K2 (propagation + RHST + surface solve + intensities) for all
+121 points.
+
+  value    points/s with inputs resident in HBM (plan created once; CUDA events
+           on the launching stream around K1+K2; L2 flushed between steps)
+  e2e      points/s through the reference-facing C-ABI call mb_rocking_curve
+           with host buffers (plan build, H2D, kernels, D2H inside the region)
+  roofline FP64 DMMA-bound propagation kernel: algorithmic flops
+           (L * 11 * 8 N^3 per point) / mean launch time vs the
+           measured DMMA peak (profiles/fp64_peak_r01.json)
+
+Multi-GPU (torchrun): every rank solves its own config-1 batch (weak scaling,
+no collective on the data path); the step time is the max over ranks.
+`--impl reference` times the CPU restatement of the reference (oracle/,
+std::thread pool over rows as sweep.cpp:111-138) on rank 0 only.
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "rocking-curve points/sec (structure x angle, fp64)"
+UNIT = "points/s"
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+def workload(args):
+    from paper_2306_00271_b200 import configs
+    if args.config == 1:
+        return configs.config1()
+    if args.config == 0:
+        return configs.config0()
+    if args.config == 2:
+        return configs.config2()
+    if args.config == 3:
+        return configs.config3()
+    return configs.config4(args.n_rods, args.method or "rk4")
+
+
+def s_eff(method):
+    return {"rk4": 4, "sp4": 6, "sp6": 11}[method]
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device, self.proc, self.path = device, None, f"/tmp/mb_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        self.proc.wait()
+        rows = []
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 7:
+                try:
+                    rows.append((float(f[0]), float(f[1]), f[3:7]))
+                except ValueError:
+                    pass
+        if not rows:
+            return None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, r in rows for i, v in enumerate(r) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def fp64_peak():
+    p = os.path.join(ROOT, "profiles", "fp64_peak_r01.json")
+    try:
+        return float(json.load(open(p))["fp64_dmma_tflops"]), "profiles/fp64_peak_r01.json (own DMMA microbenchmark; " \
+                                                              "MEASURED_PEAKS.json has no FP64 entry)"
+    except Exception:
+        return 37.1, "fallback 37.1 TF/s (own DMMA measurement, round 1)"
+
+
+def ncu_traffic(name):
+    p = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
+    try:
+        return json.load(open(p)).get(name, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def cpu_baseline(w, seconds_hint=True):
+    """Oracle (CPU restatement, reference threading) on a bounded sample."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle", "_build"))
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import mb_oracle  # checker / baseline only
+    import harness as H
+    cores = os.cpu_count() or 1
+    nang = min(len(w.theta0), cores)
+    sub = w.subset(structures=[0], theta0=w.theta0[:: max(1, len(w.theta0) // nang)][:nang])
+    t0 = time.perf_counter()
+    H.run_oracle(mb_oracle, sub, threads=0)
+    dt = time.perf_counter() - t0
+    pts = sub.points()
+    return {"value": pts / dt, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{pts} points of {w.name} (structure 0, every {max(1, len(w.theta0) // nang)}th angle), "
+                      f"{dt:.2f} s, threads=hardware_concurrency, oracle/mb_oracle.cpp -O3 no -march"}
+
+
+def run_reference(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return 0
+    w = workload(args)
+    for _ in range(args.warmup):
+        cpu_baseline(w)
+    vals = [cpu_baseline(w) for _ in range(args.steps)]
+    v = statistics.median(x["value"] for x in vals)
+    cb = dict(vals[0])
+    cb["value"] = v
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1000.0 * w.points() / v, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": w.name, "points": w.points(), "n_rods": w.n_rods, "method": w.method,
+                       "slices": w.slices},
+            "cpu_baseline": cb, "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--n-rods", type=int, default=63)
+    ap.add_argument("--method", default=None)
+    ap.add_argument("--no-fsal", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    rank, local_rank, world = dist_env()
+    import torch
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    import paper_2306_00271_b200 as mb
+    from paper_2306_00271_b200 import configs
+
+    w = workload(args)
+    method = args.method or w.method
+    if args.method:
+        w.method = method
+    ctx = mb.Context(local_rank)
+    rods = mb.RodSet.build_first(mb.Lattice2D(w.a1, w.a2), w.n_rods)
+    opts = mb.SweepOptions(method=method, slices=w.slices, fsal=not args.no_fsal)
+    fields = configs.product_fields(w)
+    pairs = [(s, t0, t1) for s in range(len(w.structures)) for t1 in w.theta1 for t0 in w.theta0]
+    plan = mb.Plan(rods, fields, w.gamma, pairs, opts, ctx)
+    info = plan.info()
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > 126 MB L2
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        torch.cuda.synchronize()
+        plan.execute()
+    barrier()
+    clocks = Clocks(local_rank)
+    clocks.start()
+    tot = pot = prop = 0.0
+    launches = 0
+    t_wall = time.perf_counter()
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        plan.execute()
+        t = plan.timing()
+        tot += t["ms_total"]
+        pot += t["ms_potential"]
+        prop += t["ms_propagate"]
+        launches += t["launches"]
+    barrier()
+    t_wall = time.perf_counter() - t_wall
+    ck = clocks.stop()
+    eta, rho, status = plan.results()
+    rhst_mean = float(status["rhst"].mean())
+    plan.close()
+
+    ms_step = tot / args.steps
+    if dist:
+        tt = torch.tensor([ms_step], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms_step = float(tt.item())
+    points = len(pairs) * world
+    value = points / (ms_step * 1e-3)
+
+    # roofline of the dominant kernel (propagation)
+    flops_launch = len(pairs) * w.slices * s_eff(method) * 8.0 * w.n_rods ** 3
+    ms_prop = prop / args.steps
+    achieved = flops_launch / (ms_prop * 1e-3) / 1e12
+    peak, peak_src = fp64_peak()
+
+    # e2e through the reference-facing C-ABI call with host buffers
+    e2e = None
+    if not args.no_e2e and len(w.structures) == 1:
+        grid = mb.AngleGrid.validated(w.theta0, w.theta1)
+        for _ in range(max(1, args.warmup)):
+            mb.rocking_curve(fields[0], rods, w.gamma, grid, opts, ctx)
+        barrier()
+        te = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            c = mb.rocking_curve(fields[0], rods, w.gamma, grid, opts, ctx)
+            te.append(time.perf_counter() - t0)
+        tmax = statistics.mean(te)
+        if dist:
+            tt = torch.tensor([tmax], device="cuda", dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            tmax = float(tt.item())
+        e2e = {"value": points / tmax, "unit": UNIT, "h2d_bytes_per_step": info["h2d_bytes"] * world,
+               "d2h_bytes_per_step": len(pairs) * w.n_rods * (8 + 16) * world + len(pairs) * 16 * world,
+               "ms_per_step": 1000.0 * tmax, "call": "mb_rocking_curve (C-ABI, host buffers)"}
+        assert np.array_equal(c.eta, eta), "e2e path must reproduce the plan path bitwise"
+
+    if rank == 0:
+        cb = None if args.no_cpu_baseline or world > 1 else cpu_baseline(w)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": w.name, "points_per_gpu": len(pairs), "n_rods": w.n_rods, "method": method,
+                       "slices": w.slices, "energy_ev": w.energy_ev, "particle": w.particle,
+                       "fsal": opts.fsal, "rhst_threshold": opts.rhst_threshold, "residual_check": True,
+                       "l2": "flushed between steps (512 MiB write); coefficient table "
+                             f"{info['coef_bytes'] / 2**20:.1f} MiB",
+                       "parallelism": f"pairs sharded per GPU, {world} rank(s), no collective"},
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": ncu_traffic("propagate"),
+                         "kernel": f"propagate_kernel (NP={info['npad']})", "peak_source": peak_src,
+                         "flops_per_launch": flops_launch,
+                         "flops_rule": f"points * L * {s_eff(method)} * 8 N^3 (N={w.n_rods}; RHST/extraction excluded)",
+                         "ms_per_launch": ms_prop},
+            "cpu_baseline": cb, "e2e": e2e, "gpu_launches": launches,
+            "kernel_ms": {"potential": pot / args.steps, "propagate": ms_prop},
+            "rhst_per_point": rhst_mean, "wall_s_timed": t_wall, "clocks": ck,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -187,8 +187,13 @@ int mb_plan_results(mb_plan* plan, double* eta, double* rho, mb_point_status* st
  * potential kernel, propagation kernel, in milliseconds; kernel launches */
 int mb_plan_timing(const mb_plan* plan, double* ms_total, double* ms_potential,
                    double* ms_propagate, int* launches);
-/* number of node slots of the coefficient table and its device bytes */
-int mb_plan_info(const mb_plan* plan, long* slots, int* ndiff, long* coef_bytes, int* npad);
+/* node slots of the coefficient table, its device bytes, the padded kernel
+ * size and the host->device bytes the plan uploaded */
+int mb_plan_info(const mb_plan* plan, long* slots, int* ndiff, long* coef_bytes, int* npad, long* h2d_bytes);
+/* per-CTA average SM cycles by kernel phase (table wait, GEMM, kick epilogue,
+ * finite check, Gershgorin, RHST, surface solve, prologue) of the last
+ * execute; all zero unless the library was built with MB_PROFILE */
+int mb_plan_profile(const mb_plan* plan, double* cycles12);
 int mb_plan_destroy(mb_plan* plan);
 
 /* rocking_curve (sweep.hpp:37-38, sweep.cpp:54-143), stepper methods:

@@ -28,7 +28,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "libmanybeam_b200.so")
+_LIB_PATH = os.environ.get("MB_LIB") or os.path.join(_HERE, "libmanybeam_b200.so")
 
 # ----------------------------------------------------------------- errors
 
@@ -154,8 +154,9 @@ def lib():
         L.mb_plan_timing.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                      C.POINTER(C.c_double), C.POINTER(C.c_int)]
         L.mb_plan_info.argtypes = [C.c_void_p, C.POINTER(C.c_long), C.POINTER(C.c_int), C.POINTER(C.c_long),
-                                   C.POINTER(C.c_int)]
+                                   C.POINTER(C.c_int), C.POINTER(C.c_long)]
         L.mb_plan_destroy.argtypes = [C.c_void_p]
+        L.mb_plan_profile.argtypes = [C.c_void_p, C.c_void_p]
         L.mb_rocking_curve.argtypes = [C.c_void_p, C.POINTER(_Field), C.POINTER(_Rods), C.c_double, C.c_void_p,
                                        C.c_int, C.c_void_p, C.c_int, C.POINTER(_Stepper), C.POINTER(_Options),
                                        C.c_void_p, C.c_void_p, C.c_void_p]
@@ -520,9 +521,18 @@ class Plan:
         return {"ms_total": t.value, "ms_potential": p.value, "ms_propagate": q.value, "launches": n.value}
 
     def info(self):
-        s, d, b, npad = C.c_long(), C.c_int(), C.c_long(), C.c_int()
-        _check(lib().mb_plan_info(self._h, C.byref(s), C.byref(d), C.byref(b), C.byref(npad)))
-        return {"slots": s.value, "ndiff": d.value, "coef_bytes": b.value, "npad": npad.value}
+        s, d, b, npad, h2d = C.c_long(), C.c_int(), C.c_long(), C.c_int(), C.c_long()
+        _check(lib().mb_plan_info(self._h, C.byref(s), C.byref(d), C.byref(b), C.byref(npad), C.byref(h2d)))
+        return {"slots": s.value, "ndiff": d.value, "coef_bytes": b.value, "npad": npad.value, "h2d_bytes": h2d.value}
+
+    PHASES = ("table_wait", "gemm", "kick_epilogue", "rhst_gj", "gershgorin", "rhst_other", "surface", "prologue",
+              "gj_rows_pre", "gj_pivot", "gj_rows_post", "gj_sync")
+
+    def profile(self):
+        """per-CTA cycles by phase (MB_PROFILE builds only)."""
+        v = np.zeros(12)
+        _check(lib().mb_plan_profile(self._h, _ptr(v)))
+        return dict(zip(self.PHASES, v.tolist()))
 
     def close(self):
         if self._h:

@@ -411,6 +411,7 @@ struct mb_plan {
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
   float ms_total = 0, ms_pot = 0, ms_prop = 0;
   int launches = 0;
+  long h2d_bytes = 0;
   bool executed = false;
   std::vector<double2> host_coef;  // tabulated / zero fields: precomputed table
 };
@@ -423,8 +424,10 @@ T* dev_upload(mb_plan* pl, const T* src, std::size_t count) {
   b.bytes = std::max<std::size_t>(count * sizeof(T), 16);
   cuda_check(cudaMallocAsync(&b.p, b.bytes, pl->ctx->stream), "cudaMallocAsync");
   pl->bufs.push_back(b);
-  if (count && src)
+  if (count && src) {
     cuda_check(cudaMemcpyAsync(b.p, src, count * sizeof(T), cudaMemcpyHostToDevice, pl->ctx->stream), "cudaMemcpyAsync H2D");
+    pl->h2d_bytes += (long)(count * sizeof(T));
+  }
   return static_cast<T*>(b.p);
 }
 template <class T>
@@ -649,6 +652,7 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
       cuda_check(cudaMemcpyAsync(coef, pl->host_coef.data(), pl->host_coef.size() * sizeof(double2),
                                  cudaMemcpyHostToDevice, st),
                  "upload coefficient table");
+      pl->h2d_bytes += (long)(pl->host_coef.size() * sizeof(double2));
     }
 
     // ---- propagation parameters
@@ -693,6 +697,7 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
     p.eta = dev_alloc<double>(pl, (std::size_t)npairs * n);
     p.rho = dev_alloc<double2>(pl, (std::size_t)npairs * n);
     p.status = dev_alloc<mbx::PointStatus>(pl, (std::size_t)npairs);
+    p.prof = dev_alloc<unsigned long long>(pl, 12);
     for (cudaEvent_t& e : pl->ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
   } catch (...) {
     free_plan(pl);
@@ -708,6 +713,7 @@ void execute_plan(mb_plan* pl, cudaStream_t st) {
   cuda_check(cudaEventRecord(pl->ev[0], st), "event");
   if (pl->use_k1) cuda_check(mbx::launch_potential(pl->pot, st, &pl->launches), "potential kernel launch");
   cuda_check(cudaEventRecord(pl->ev[1], st), "event");
+  cuda_check(cudaMemsetAsync(pl->prop.prof, 0, 12 * sizeof(unsigned long long), st), "memset");
   int npad = 0;
   cuda_check(mbx::launch_propagate(pl->prop, st, &pl->launches, &npad), "propagation kernel launch");
   cuda_check(cudaEventRecord(pl->ev[2], st), "event");
@@ -897,13 +903,23 @@ int mb_plan_timing(const mb_plan* plan, double* ms_total, double* ms_potential, 
   });
 }
 
-int mb_plan_info(const mb_plan* plan, long* slots, int* ndiff, long* coef_bytes, int* npad) {
+int mb_plan_info(const mb_plan* plan, long* slots, int* ndiff, long* coef_bytes, int* npad, long* h2d_bytes) {
   return guarded([&] {
     if (!plan) fail(MB_ERR_ARG, "null plan");
     if (slots) *slots = plan->nslots;
     if (ndiff) *ndiff = plan->ndiff;
     if (coef_bytes) *coef_bytes = (long)plan->S * plan->nslots * plan->ndiff * (long)sizeof(double2);
     if (npad) *npad = plan->npad;
+    if (h2d_bytes) *h2d_bytes = plan->h2d_bytes;
+  });
+}
+
+int mb_plan_profile(const mb_plan* plan, double* cycles) {
+  return guarded([&] {
+    if (!plan || !cycles) fail(MB_ERR_ARG, "null argument");
+    unsigned long long v[12];
+    cuda_check(cudaMemcpy(v, plan->prop.prof, sizeof v, cudaMemcpyDeviceToHost), "D2H profile");
+    for (int q = 0; q < 12; ++q) cycles[q] = (double)v[q] / (double)plan->npairs;
   });
 }
 

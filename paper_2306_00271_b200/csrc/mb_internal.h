@@ -69,6 +69,7 @@ struct PropagateParams {
   double* eta;                // [npairs][n]
   double2* rho;               // [npairs][n]
   PointStatus* status;        // [npairs]
+  unsigned long long* prof;   // [8] phase cycles (MB_PROFILE builds), may be null
 };
 
 // launchers (mb_kernels.cu)

@@ -25,6 +25,21 @@
 namespace mbx {
 
 // ============================================================== helpers
+// MB_PROFILE builds (make prof) accumulate per-phase SM cycles of thread 0 of
+// every CTA: 0 table wait+barrier, 1 GEMM, 2 kick epilogue, 3 RHST Gauss-Jordan,
+// 4 Gershgorin, 5 RHST, 6 surface solve, 7 prologue.
+#ifdef MB_PROFILE
+#define PROF_MARK(slot)                             \
+  do {                                              \
+    const long long _t = clock64();                 \
+    prof_acc[slot] += _t - prof_t;                  \
+    prof_t = _t;                                    \
+  } while (0)
+#else
+#define PROF_MARK(slot) \
+  do {                  \
+  } while (0)
+#endif
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
       : "+d"(c0), "+d"(c1)
@@ -215,6 +230,31 @@ __device__ __forceinline__ void zero(double (&v)[C::MB][C::NB][4]) {
       for (int q = 0; q < 4; ++q) v[mb][nb][q] = 0.0;
 }
 
+// complex 8x8x4 block products: re += ar*br - ai*bi, im += ar*bi + ai*br.
+// Issue order keeps the two updates of one accumulator 2*MB*NB DMMAs apart so
+// the DMMA latency is hidden (back-to-back dependent DMMAs stall the warp).
+template <class C>
+__device__ __forceinline__ void cmma(double (&acc)[C::MB][C::NB][4], const double (&ar)[C::MB],
+                                     const double (&ai)[C::MB], const double (&an)[C::MB], const double (&br)[C::NB],
+                                     const double (&bi)[C::NB]) {
+#pragma unroll
+  for (int mb = 0; mb < C::MB; ++mb)
+#pragma unroll
+    for (int nb = 0; nb < C::NB; ++nb) dmma(acc[mb][nb][0], acc[mb][nb][1], ar[mb], br[nb]);
+#pragma unroll
+  for (int mb = 0; mb < C::MB; ++mb)
+#pragma unroll
+    for (int nb = 0; nb < C::NB; ++nb) dmma(acc[mb][nb][2], acc[mb][nb][3], ar[mb], bi[nb]);
+#pragma unroll
+  for (int mb = 0; mb < C::MB; ++mb)
+#pragma unroll
+    for (int nb = 0; nb < C::NB; ++nb) dmma(acc[mb][nb][0], acc[mb][nb][1], an[mb], bi[nb]);
+#pragma unroll
+  for (int mb = 0; mb < C::MB; ++mb)
+#pragma unroll
+    for (int nb = 0; nb < C::NB; ++nb) dmma(acc[mb][nb][2], acc[mb][nb][3], ai[mb], br[nb]);
+}
+
 // acc = U * X, U gathered from the node's box table: U(j,k) = box[raddr_j - off_k]
 // (raddr_j = center + off_j, or -1 for padded rows -> 0). X rows k >= n are zero
 // by construction, so padded columns of U need no mask.
@@ -245,15 +285,7 @@ __device__ __forceinline__ void gemm_box(double (&acc)[C::MB][C::NB][4], const d
       br[nb] = Xr[o];
       bi[nb] = Xi[o];
     }
-#pragma unroll
-    for (int mb = 0; mb < C::MB; ++mb)
-#pragma unroll
-      for (int nb = 0; nb < C::NB; ++nb) {
-        dmma(acc[mb][nb][0], acc[mb][nb][1], ar[mb], br[nb]);
-        dmma(acc[mb][nb][0], acc[mb][nb][1], an[mb], bi[nb]);
-        dmma(acc[mb][nb][2], acc[mb][nb][3], ar[mb], bi[nb]);
-        dmma(acc[mb][nb][2], acc[mb][nb][3], ai[mb], br[nb]);
-      }
+    cmma<C>(acc, ar, ai, an, br, bi);
   }
 }
 
@@ -282,15 +314,7 @@ __device__ __forceinline__ void gemm_dense(double (&acc)[C::MB][C::NB][4], const
       br[nb] = Xr[o];
       bi[nb] = Xi[o];
     }
-#pragma unroll
-    for (int mb = 0; mb < C::MB; ++mb)
-#pragma unroll
-      for (int nb = 0; nb < C::NB; ++nb) {
-        dmma(acc[mb][nb][0], acc[mb][nb][1], ar[mb], br[nb]);
-        dmma(acc[mb][nb][0], acc[mb][nb][1], an[mb], bi[nb]);
-        dmma(acc[mb][nb][2], acc[mb][nb][3], ar[mb], bi[nb]);
-        dmma(acc[mb][nb][2], acc[mb][nb][3], ai[mb], br[nb]);
-      }
+    cmma<C>(acc, ar, ai, an, br, bi);
   }
 }
 
@@ -298,40 +322,82 @@ __device__ __forceinline__ void gemm_dense(double (&acc)[C::MB][C::NB][4], const
 struct Scratch {
   double red_a[32], red_b[32];
   int red_i[32];
-  int piv;
-  double pivval;
-  double2 inv;
+  int piv[2];
+  double pivval[2];
+  double2 inv[2];
 };
 
-// Gershgorin condition estimate of the n x n block of Q (kernels.cpp:82-99):
-// max_i(|q_ii| + r_i) / min_i(|q_ii| - r_i), +inf if any |q_ii| - r_i <= 0.
+__device__ __forceinline__ double inf_d() { return __longlong_as_double(0x7ff0000000000000LL); }
+
+// End-of-step check on own elements, fused (proposed.cpp:279-287 +
+// kernels.cpp:82-99): returns -1 if Q or P holds a nonfinite value, else the
+// Gershgorin estimate max_i(|q_ii| + r_i) / min_i(|q_ii| - r_i) (+inf when
+// some |q_ii| - r_i <= 0). Row sums are reduced in the accumulator layout:
+// quad shuffles, then the WN column-warps through shared memory.
 template <class C>
-__device__ double gershgorin(const double* Qr, const double* Qi, int n, Scratch& sc, int warp, int lane) {
-  double hi = 0.0, lo = __longlong_as_double(0x7ff0000000000000LL);
+__device__ double finite_and_gershgorin(const double* Qr, const double* Qi, const double (&P)[C::MB][C::NB][4],
+                                        const Own<C>& own, int n, double* rsum /*[WN][NP]*/,
+                                        double* dsum /*[WN][NP]*/, Scratch& sc, int tid, int warp, int lane) {
   int bad = 0;
-  for (int i = warp; i < n; i += C::NW) {
-    double rs = 0.0, dg = 0.0;
-    for (int j = lane; j < n; j += 32) {
-      const int o = sw<C::NP>(i, j);
-      const double a = hypot(Qr[o], Qi[o]);
-      if (j == i)
-        dg = a;
-      else
-        rs += a;
+  double rs[C::MB], dg[C::MB];
+#pragma unroll
+  for (int mb = 0; mb < C::MB; ++mb) {
+    rs[mb] = 0.0;
+    dg[mb] = 0.0;
+    const int r = own.r(mb);
+#pragma unroll
+    for (int nb = 0; nb < C::NB; ++nb) {
+      double q[4];
+      own.ld(Qr, Qi, mb, nb, q);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = own.c(nb) + e;
+        bad |= !isfinite(q[e]) || !isfinite(q[2 + e]) || !isfinite(P[mb][nb][e]) || !isfinite(P[mb][nb][2 + e]);
+        const double a = sqrt(q[e] * q[e] + q[2 + e] * q[2 + e]);
+        if (c == r)
+          dg[mb] = a;
+        else if (c < n)
+          rs[mb] += a;
+      }
     }
-    rs = warp_sum(rs);
-    dg = warp_sum(dg);
-    hi = fmax(hi, dg + rs);
-    if (dg - rs <= 0.0) bad = 1;
-    lo = fmin(lo, dg - rs);
+    rs[mb] += __shfl_xor_sync(0xffffffffu, rs[mb], 1);
+    rs[mb] += __shfl_xor_sync(0xffffffffu, rs[mb], 2);
+    dg[mb] += __shfl_xor_sync(0xffffffffu, dg[mb], 1);
+    dg[mb] += __shfl_xor_sync(0xffffffffu, dg[mb], 2);
+    if ((lane & 3) == 0) {
+      const int wn = own.col0 / C::TN;
+      rsum[wn * C::NP + r] = rs[mb];
+      dsum[wn * C::NP + r] = dg[mb];
+    }
+  }
+  bad = __syncthreads_or(bad);
+  if (bad) return -1.0;
+  double hi = 0.0, lo = inf_d();
+  int nd = 0;
+  for (int i = tid; i < n; i += C::NT) {
+    double r = 0.0, d = 0.0;
+#pragma unroll
+    for (int w = 0; w < C::WN; ++w) {
+      r += rsum[w * C::NP + i];
+      d += dsum[w * C::NP + i];
+    }
+    hi = fmax(hi, d + r);
+    if (d - r <= 0.0) nd = 1;
+    lo = fmin(lo, d - r);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    nd |= __shfl_xor_sync(0xffffffffu, nd, o);
   }
   if (lane == 0) {
     sc.red_a[warp] = hi;
     sc.red_b[warp] = lo;
-    sc.red_i[warp] = bad;
+    sc.red_i[warp] = nd;
   }
   __syncthreads();
-  double H = 0.0, L = __longlong_as_double(0x7ff0000000000000LL);
+  double H = 0.0, L = inf_d();
   int B = 0;
 #pragma unroll
   for (int w = 0; w < C::NW; ++w) {
@@ -339,105 +405,212 @@ __device__ double gershgorin(const double* Qr, const double* Qi, int n, Scratch&
     L = fmin(L, sc.red_b[w]);
     B |= sc.red_i[w];
   }
-  __syncthreads();  // scratch reusable
   if (n == 0) return 1.0;
-  if (B) return __longlong_as_double(0x7ff0000000000000LL);
+  if (B) return inf_d();
   return H / L;
 }
 
-// B <- B * A^-1 for the n x n blocks (A destroyed): Gauss-Jordan column
-// elimination with partial pivoting on row k of A (== Eigen PartialPivLU of
-// A^T pivoting on column k, first maximum wins; kernels.cpp:66-71).
-// Returns false on an exactly zero pivot (kernels.cpp:68-71).
+// Pivot of row k for the Gauss-Jordan step: first maximum of |A[k][j]| over
+// j >= k (Eigen's abs score; compared as |a|^2, which orders identically up to
+// ties within one rounding), multipliers f_j of the post-swap row, 1/pivot.
+// `a` holds the lane's row-k elements (j = lane + 32 q).
 template <class C>
-__device__ bool gauss_jordan(double* Ar, double* Ai, double* Br, double* Bi, double2* fv, int n, Scratch& sc,
-                             int tid, int warp, int lane) {
-  for (int k = 0; k < n; ++k) {
-    if (warp == 0) {
-      double best = -1.0;
-      int bj = n;
-      for (int j = k + lane; j < n; j += 32) {
-        const int o = sw<C::NP>(k, j);
-        const double v = hypot(Ar[o], Ai[o]);
-        if (v > best) {
-          best = v;
-          bj = j;
-        }
-      }
+__device__ __forceinline__ void gj_pivot(const double2 (&a)[(C::NP + 31) / 32], int k, int n, double2* fv,
+                                         Scratch& sc, int slot, int lane) {
+  constexpr int NQ = (C::NP + 31) / 32;
+  // lane-local first maximum of |a|^2 (q ascending = j ascending)
+  double best = -1.0;
+  int bj = n;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
-        if (ob > best || (ob == best && oj < bj)) {
-          best = ob;
-          bj = oj;
-        }
-      }
-      const int p = bj;
-      // multipliers of the post-swap row k: f_j = A[k][j] (j != k)
-      for (int j = lane; j < n; j += 32) {
-        double2 f = make_double2(0.0, 0.0);
-        if (j != k) {
-          const int src = (j == p) ? k : j;
-          const int o = sw<C::NP>(k, src);
-          f = make_double2(Ar[o], Ai[o]);
-        }
-        fv[j] = f;
-      }
-      if (lane == 0) {
-        sc.piv = p;
-        sc.pivval = best;
-        const int o = sw<C::NP>(k, p);
-        sc.inv = best > 0.0 ? cinv(make_double2(Ar[o], Ai[o])) : make_double2(0.0, 0.0);
+  for (int q = 0; q < NQ; ++q) {
+    const int j = lane + 32 * q;
+    const double v = a[q].x * a[q].x + a[q].y * a[q].y;
+    if (j >= k && j < n && v > best) {
+      best = v;
+      bj = j;
+    }
+  }
+  // warp maximum: 32-bit key (float(|a|^2) bits are monotone for v >= 0; -1
+  // maps to 0), exact double comparison only among lanes tied on the key
+  const unsigned key = best < 0.0 ? 0u : __float_as_uint(__double2float_ru(best)) + 1u;
+  const unsigned kmax = __reduce_max_sync(0xffffffffu, key);
+  const unsigned tied = __ballot_sync(0xffffffffu, key == kmax);
+  if (__popc(tied) > 1) {
+    double b = key == kmax ? best : -1.0;
+    int jj = key == kmax ? bj : n;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, b, o);
+      const int oj = __shfl_xor_sync(0xffffffffu, jj, o);
+      if (ob > b || (ob == b && oj < jj)) {
+        b = ob;
+        jj = oj;
       }
     }
-    __syncthreads();
-    if (!(sc.pivval > 0.0)) return false;
-    const int p = sc.piv;
-    const double2 inv = sc.inv;
-    for (int i = tid; i < n; i += C::NT) {
-      const int ok = sw<C::NP>(i, k), op = sw<C::NP>(i, p);
-      double2 a = make_double2(Ar[op], Ai[op]);
-      double2 b = make_double2(Br[op], Bi[op]);
-      if (p != k) {
-        Ar[op] = Ar[ok];
-        Ai[op] = Ai[ok];
-        Br[op] = Br[ok];
-        Bi[op] = Bi[ok];
-      }
-      a = cmul(a, inv);
-      b = cmul(b, inv);
-      Ar[ok] = a.x;
-      Ai[ok] = a.y;
-      Br[ok] = b.x;
-      Bi[ok] = b.y;
+    best = b;
+    bj = jj;
+  } else {
+    const int src = __ffs(tied) - 1;
+    best = __shfl_sync(0xffffffffu, best, src);
+    bj = __shfl_sync(0xffffffffu, bj, src);
+  }
+  const int p = bj;
+  double2 akk = make_double2(0.0, 0.0), akp = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const double2 x = make_double2(__shfl_sync(0xffffffffu, a[q].x, k & 31), __shfl_sync(0xffffffffu, a[q].y, k & 31));
+    const double2 y = make_double2(__shfl_sync(0xffffffffu, a[q].x, p & 31), __shfl_sync(0xffffffffu, a[q].y, p & 31));
+    if (q == (k >> 5)) akk = x;
+    if (q == (p >> 5)) akp = y;
+  }
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const int j = lane + 32 * q;
+    if (j < C::NP) fv[j] = (j == k || j >= n) ? make_double2(0.0, 0.0) : (j == p ? akk : a[q]);
+  }
+  if (lane == 0) {
+    sc.piv[slot] = p;
+    sc.pivval[slot] = best;
+    // 1/|pivot|^2: RCP64H seed + two Newton steps (inverse by multiplication,
+    // like any reciprocal-scaled elimination; rounding-level only)
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(best));
+    r = r * fma(-best, r, 2.0);
+    r = r * fma(-best, r, 2.0);
+    sc.inv[slot] = best > 0.0 ? make_double2(akp.x * r, -akp.y * r) : make_double2(0.0, 0.0);
+  }
+}
+
+// Gauss-Jordan row update: X[i][:] for the elimination of column k with
+// pivot column p (new column k = X[i][p] * inv; column p takes old column k).
+// Branch-free (clamped rows, value selects, predicated stores) so the loads of
+// all RB rows issue before any arithmetic.
+template <class C, int RB>
+__device__ __forceinline__ void gj_rows(double* Ar, double* Ai, double* Br, double* Bi, const int (&rows)[RB],
+                                        const bool (&isA)[RB], int k, int p, double2 inv,
+                                        const double2 (&fj)[(C::NP + 31) / 32], double2 (&row)[RB][(C::NP + 31) / 32],
+                                        int lane) {
+  constexpr int NQ = (C::NP + 31) / 32;
+  double2 xv[RB], ok_[RB];
+  int base[RB];
+  double* pr[RB];
+  double* pi[RB];
+#pragma unroll
+  for (int u = 0; u < RB; ++u) {
+    const int i = rows[u] < 0 ? 0 : rows[u];
+    pr[u] = isA[u] ? Ar : Br;
+    pi[u] = isA[u] ? Ai : Bi;
+    base[u] = i;
+    xv[u] = make_double2(pr[u][sw<C::NP>(i, p)], pi[u][sw<C::NP>(i, p)]);
+    ok_[u] = make_double2(pr[u][sw<C::NP>(i, k)], pi[u][sw<C::NP>(i, k)]);
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int j = (lane + 32 * q) & (C::NP - 1);
+      row[u][q] = make_double2(pr[u][sw<C::NP>(i, j)], pi[u][sw<C::NP>(i, j)]);
     }
-    __syncthreads();
-    // eliminate: col_j -= f_j col_k for j != k. A rows < k are final (unit) and
-    // never read again; B needs every row.
-    const int rowsA = n - k;
-    const int work = (rowsA + n) * n;
-    for (int w = tid; w < work; w += C::NT) {
-      const int i2 = w / n, j = w % n;
-      if (j == k) continue;
-      const double2 f = fv[j];
-      if (i2 < rowsA) {
-        const int i = k + i2;
-        const double2 x = make_double2(Ar[sw<C::NP>(i, k)], Ai[sw<C::NP>(i, k)]);
-        const int o = sw<C::NP>(i, j);
-        Ar[o] -= f.x * x.x - f.y * x.y;
-        Ai[o] -= f.x * x.y + f.y * x.x;
-      } else {
-        const int i = i2 - rowsA;
-        const double2 x = make_double2(Br[sw<C::NP>(i, k)], Bi[sw<C::NP>(i, k)]);
-        const int o = sw<C::NP>(i, j);
-        Br[o] -= f.x * x.x - f.y * x.y;
-        Bi[o] -= f.x * x.y + f.y * x.x;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int u = 0; u < RB; ++u) {
+    const double2 x = cmul(xv[u], inv);
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int j = lane + 32 * q;
+      const double2 v = (j == p) ? ok_[u] : row[u][q];
+      double2 nv = make_double2(v.x - (fj[q].x * x.x - fj[q].y * x.y), v.y - (fj[q].x * x.y + fj[q].y * x.x));
+      nv = (j == k) ? x : nv;
+      row[u][q] = nv;
+      if (rows[u] >= 0 && j < C::NP) {
+        const int o = sw<C::NP>(base[u], j);
+        pr[u][o] = nv.x;
+        pi[u][o] = nv.y;
       }
     }
+  }
+}
+
+// B <- B * A^-1 on the n x n blocks (A destroyed): Gauss-Jordan column
+// elimination with partial pivoting on row k of A. This is Eigen's
+// PartialPivLU of A^T (kernels.cpp:66-71: row pivoting of A^T = column
+// pivoting here, first maximum wins) fused with the substitution. Warp 0
+// updates row k+1 of A first and immediately computes the next pivot (the
+// only serial chain); every warp then updates the remaining rows in batches.
+// One barrier per pivot step. Returns false on an exactly zero pivot
+// (kernels.cpp:68-71).
+template <class C, int RB_ = 0>
+__device__ bool gauss_jordan(double* Ar, double* Ai, double* Br, double* Bi, double2* fv /*[2][NP]*/, int n,
+                             Scratch& sc, int warp, int lane, long long* pa = nullptr) {
+#ifdef MB_PROFILE
+  long long t_prev = clock64();
+#define GJ_MARK(q)                    \
+  do {                                \
+    if (pa) {                         \
+      const long long _t = clock64(); \
+      pa[q] += _t - t_prev;           \
+      t_prev = _t;                    \
+    }                                 \
+  } while (0)
+#else
+#define GJ_MARK(q) \
+  do {             \
+  } while (0)
+#endif
+  constexpr int NQ = (C::NP + 31) / 32;
+  constexpr int RB = RB_ ? RB_ : (NQ == 1 ? 8 : 4);  // rows per batch (register budget: P stays live)
+  if (n == 0) return true;
+  if (warp == 0) {
+    double2 a[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int j = lane + 32 * q;
+      a[q] = j < C::NP ? make_double2(Ar[sw<C::NP>(0, j)], Ai[sw<C::NP>(0, j)]) : make_double2(0.0, 0.0);
+    }
+    gj_pivot<C>(a, 0, n, fv, sc, 0, lane);
+  }
+  __syncthreads();
+  for (int k = 0; k < n; ++k) {
+    const int slot = k & 1;
+    if (!(sc.pivval[slot] > 0.0)) return false;
+    const int p = sc.piv[slot];
+    const double2 inv = sc.inv[slot];
+    const double2* f = fv + slot * C::NP;
+    double2 fj[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int j = lane + 32 * q;
+      fj[q] = j < C::NP ? f[j] : make_double2(0.0, 0.0);
+    }
+    GJ_MARK(11);
+    if (warp == 0 && k + 1 < n) {  // critical chain: row k+1, then the next pivot
+      const int rows[1] = {k + 1};
+      const bool isA[1] = {true};
+      double2 row[1][NQ];
+      gj_rows<C, 1>(Ar, Ai, Br, Bi, rows, isA, k, p, inv, fj, row, lane);
+      GJ_MARK(8);
+      gj_pivot<C>(row[0], k + 1, n, fv + (slot ^ 1) * C::NP, sc, slot ^ 1, lane);
+      GJ_MARK(9);
+    }
+    // remaining rows: A rows k+2..n-1, B rows 0..n-1, over the warps that are
+    // not on the pivot chain
+    constexpr int W0 = C::NW > 1 ? 1 : 0, NWP = C::NW - W0;
+    const int nA = n > k + 2 ? n - k - 2 : 0, total = nA + n;
+    for (int t0 = warp - W0; t0 >= 0 && t0 < total; t0 += RB * NWP) {
+      int rows[RB];
+      bool isA[RB];
+#pragma unroll
+      for (int u = 0; u < RB; ++u) {
+        const int t = t0 + u * NWP;
+        isA[u] = t < nA;
+        rows[u] = t >= total ? -1 : (t < nA ? k + 2 + t : t - nA);
+      }
+      double2 row[RB][NQ];
+      gj_rows<C, RB>(Ar, Ai, Br, Bi, rows, isA, k, p, inv, fj, row, lane);
+    }
+    GJ_MARK(10);
     __syncthreads();
   }
   return true;
+#undef GJ_MARK
 }
 
 // identity on the n x n block, zero elsewhere
@@ -451,16 +624,13 @@ __device__ void set_identity(double* Xr, double* Xi, int n, int tid) {
 }
 
 // solve_right residual gate (kernels.cpp:73-79): ||X A0 - B0||_F / ||B0||_F <= 1e-10.
-// X dense in (Xr, Xi); A0 own elements in a0 (written into (Ar, Ai) first);
-// B0 own elements in b0.
-template <class C>
-__device__ bool residual_ok(double* Ar, double* Ai, const double* Xr, const double* Xi,
-                            const double (&a0)[C::MB][C::NB][4], const double (&b0)[C::MB][C::NB][4],
+// X dense in (Xr, Xi), A0 dense in (Or, Oi); B0 element (mb, nb, q) of the
+// calling thread is produced by `b0`.
+template <class C, class F>
+__device__ bool residual_ok(const double* Or, const double* Oi, const double* Xr, const double* Xi, F&& b0,
                             double (&acc)[C::MB][C::NB][4], const Own<C>& own, int n, Scratch& sc, int warp,
                             int lane) {
-  own.store(Ar, Ai, a0);
-  __syncthreads();
-  gemm_dense<C>(acc, Xr, Xi, Ar, Ai, own.row0, own.col0, lane, (n + 3) & ~3);
+  gemm_dense<C>(acc, Xr, Xi, Or, Oi, own.row0, own.col0, lane, (n + 3) & ~3);
   double rn = 0.0, bn = 0.0, bad = 0.0;
 #pragma unroll
   for (int mb = 0; mb < C::MB; ++mb)
@@ -468,9 +638,10 @@ __device__ bool residual_ok(double* Ar, double* Ai, const double* Xr, const doub
     for (int nb = 0; nb < C::NB; ++nb)
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const double d = acc[mb][nb][q] - b0[mb][nb][q];
+        const double t = b0(mb, nb, q);
+        const double d = acc[mb][nb][q] - t;
         rn += d * d;
-        bn += b0[mb][nb][q] * b0[mb][nb][q];
+        bn += t * t;
         if (!isfinite(acc[mb][nb][q])) bad = 1.0;
       }
   rn = warp_sum(rn);
@@ -500,19 +671,21 @@ template <class C, bool RK4>
 __global__ void __launch_bounds__(C::NT, 1) propagate_kernel(const __grid_constant__ PropagateParams p) {
   constexpr int NP = C::NP, MB = C::MB, NB = C::NB;
   extern __shared__ __align__(16) unsigned char smem[];
-  double* Ar = reinterpret_cast<double*>(smem);
-  double* Ai = Ar + NP * NP;
-  double* Br = Ai + NP * NP;
-  double* Bi = Br + NP * NP;
-  double* Cr = Bi + NP * NP;  // RK4 only
-  double* Ci = Cr + NP * NP;
-  double2* box0 = reinterpret_cast<double2*>(RK4 ? Ci + NP * NP : Cr);
+  // planes: splitting uses X0/X1 as ping-pong Q buffers (the free one is the
+  // RHST scratch) and X2 for the residual gate's saved copy; RK4 uses
+  // X0 = Q, X1 = X2/X4 (scratch at step end), X2 = X3 (saved copy).
+  double* const base = reinterpret_cast<double*>(smem);
+  double* const Xr[3] = {base, base + 2 * NP * NP, base + 4 * NP * NP};
+  double* const Xi[3] = {base + NP * NP, base + 3 * NP * NP, base + 5 * NP * NP};
+  double2* box0 = reinterpret_cast<double2*>(reinterpret_cast<double*>(smem) + 6 * NP * NP);
   double2* box1 = box0 + p.box_size;
-  double2* fv = box1 + p.box_size;           // [NP]
-  double* g2s = reinterpret_cast<double*>(fv + NP);  // [NP]
-  int* soff = reinterpret_cast<int*>(g2s + NP);      // [NP]
+  double2* fv = box1 + p.box_size;                     // [2][NP]
+  double* g2s = reinterpret_cast<double*>(fv + 2 * NP);  // [NP]
+  double* rsum = g2s + NP;                              // [WN][NP]
+  double* dsum = rsum + C::WN * NP;                     // [WN][NP]
+  int* soff = reinterpret_cast<int*>(dsum + C::WN * NP);  // [NP]
   Scratch* sc = reinterpret_cast<Scratch*>(soff + NP);
-  int* sboxpos = reinterpret_cast<int*>(sc + 1);     // [ndiff]
+  int* sboxpos = reinterpret_cast<int*>(sc + 1);  // [ndiff]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = p.n;
@@ -521,7 +694,15 @@ __global__ void __launch_bounds__(C::NT, 1) propagate_kernel(const __grid_consta
   Own<C> own{wm * C::TM, wn * C::TN, lane};
   const double2* coef = p.coef + (long)p.pair_struct[pair] * p.nslots * p.ndiff;
   const int kmax = (n + 3) & ~3;
+#ifdef MB_PROFILE
+  long long prof_t = clock64(), prof_acc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+#endif
 
+  // current / next Q planes (pointer swap, never a runtime-indexed array)
+  double* Ar = Xr[0];
+  double* Ai = Xi[0];
+  double* Nr = Xr[1];
+  double* Ni = Xi[1];
   for (int i = tid; i < p.ndiff; i += C::NT) sboxpos[i] = p.boxpos[i];
   for (int i = tid; i < NP; i += C::NT) {
     soff[i] = i < n ? p.rowoff[i] : 0;
@@ -559,9 +740,8 @@ __global__ void __launch_bounds__(C::NT, 1) propagate_kernel(const __grid_consta
 
   double acc[MB][NB][4];
   double SQ[RK4 ? MB : 1][RK4 ? NB : 1][4];
-  double SAVE[MB][NB][4];
 
-  // table pipeline: occurrence o = step * nocc + r; slot = step*stride + node
+  // table pipeline: slot of occurrence (step, r) = step*stride + node
   auto slot_of = [&](int step, int r) -> long { return (long)step * p.slot_stride + p.occ_node[r]; };
   auto issue = [&](double2* dst, long slot) {
     const double2* src = coef + slot * p.ndiff;
@@ -571,8 +751,7 @@ __global__ void __launch_bounds__(C::NT, 1) propagate_kernel(const __grid_consta
   double2* cur = box0;
   double2* nxt = box1;
   __syncthreads();  // sboxpos ready
-  const int r_first = 0;
-  long cur_slot = slot_of(0, r_first);
+  long cur_slot = slot_of(0, 0);
   issue(cur, cur_slot);
 
   int rhst = 0;
@@ -581,18 +760,16 @@ __global__ void __launch_bounds__(C::NT, 1) propagate_kernel(const __grid_consta
   const int L = p.nsteps;
   const bool fsal = !RK4 && p.fsal && p.variant == 1;
 
-  // advance the table pipeline to occurrence (step, r); returns the box to use
-  auto begin_occ = [&](int step, int r, int nstep, int nr) -> double2* {
+  // Barrier that publishes the previous phase's shared-memory writes and the
+  // table of occurrence (step, r); prefetches the next occurrence's table.
+  auto begin_occ = [&](int nstep, int nr) -> double2* {
+    PROF_MARK(2);
     cp_async_wait_all();
     __syncthreads();
+    PROF_MARK(0);
     if (nstep < L) {
       const long ns = slot_of(nstep, nr);
-      if (ns != cur_slot) {
-        issue(nxt, ns);
-        double2* b = cur;
-        // current box stays `cur` for this occurrence; swap after use
-        (void)b;
-      }
+      if (ns != cur_slot) issue(nxt, ns);
     }
     return cur;
   };
@@ -609,37 +786,47 @@ __global__ void __launch_bounds__(C::NT, 1) propagate_kernel(const __grid_consta
   };
 
 #define FOR_BLK _Pragma("unroll") for (int mb = 0; mb < MB; ++mb) _Pragma("unroll") for (int nb = 0; nb < NB; ++nb)
-  // Q += c * P on own elements (caller orders the other warps' reads of A)
-  auto drift = [&](double c) {
+  // splitting drift into the other Q buffer: Qn = Q + c P (own elements); no
+  // write-after-read hazard with warps still reading Q in their GEMM.
+  auto drift_swap = [&](double c) {
     FOR_BLK {
       double q0[4];
       own.ld(Ar, Ai, mb, nb, q0);
 #pragma unroll
       for (int q = 0; q < 4; ++q) q0[q] += c * P[mb][nb][q];
-      own.st(Ar, Ai, mb, nb, q0);
+      own.st(Nr, Ni, mb, nb, q0);
     }
+    double* t = Ar;
+    Ar = Nr;
+    Nr = t;
+    t = Ai;
+    Ai = Ni;
+    Ni = t;
   };
+  PROF_MARK(7);
   for (int step = 0; step < L; ++step) {
     if constexpr (RK4) {
       // ---------------- classical RK4 (proposed.cpp:141-168), restructured:
       // Qnew = Q + hP + h^2/6 (K1+K2+K3), Pnew = P + h/6 (K1 + 2K2 + 2K3 + K4),
       // X2 = Q + h/2 P, X3 = X2 + h^2/4 K1, X4 = Q + hP + h^2/2 K2, K = -(U+G^2) X
       const double h = p.h;
-      FOR_BLK {  // B = X2 = Q + h/2 P
+      double *Qr = Xr[0], *Qi = Xi[0], *Yr = Xr[1], *Yi = Xi[1], *Zr = Xr[2], *Zi = Xi[2];
+      FOR_BLK {  // Y = X2 = Q + h/2 P
         double v[4];
-        own.ld(Ar, Ai, mb, nb, v);
+        own.ld(Qr, Qi, mb, nb, v);
 #pragma unroll
         for (int q = 0; q < 4; ++q) v[q] += (0.5 * h) * P[mb][nb][q];
-        own.st(Br, Bi, mb, nb, v);
+        own.st(Yr, Yi, mb, nb, v);
       }
-      // stage 1 (foot) on Q (A)
-      double2* box = begin_occ(step, 0, step, 1);
-      gemm_box<C>(acc, box, soff, raddr, Ar, Ai, own.col0, lane, kmax);
+      // stage 1 (foot) on Q
+      double2* box = begin_occ(step, 1);
+      gemm_box<C>(acc, box, soff, raddr, Qr, Qi, own.col0, lane, kmax);
+      PROF_MARK(1);
       end_occ(step, 1);
       FOR_BLK {
         double q0[4], x2[4];
-        own.ld(Ar, Ai, mb, nb, q0);
-        own.ld(Br, Bi, mb, nb, x2);
+        own.ld(Qr, Qi, mb, nb, q0);
+        own.ld(Yr, Yi, mb, nb, x2);
         const double g2 = g2s[own.r(mb)];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -648,26 +835,27 @@ __global__ void __launch_bounds__(C::NT, 1) propagate_kernel(const __grid_consta
           SQ[mb][nb][q] = K;
           x2[q] += (0.25 * h * h) * K;  // X3
         }
-        own.st(Cr, Ci, mb, nb, x2);
+        own.st(Zr, Zi, mb, nb, x2);
       }
-      __syncthreads();  // every warp finished reading A in the stage-1 GEMM
+      __syncthreads();  // every warp finished reading Q in the stage-1 GEMM
       FOR_BLK {
         double q0[4];
-        own.ld(Ar, Ai, mb, nb, q0);
+        own.ld(Qr, Qi, mb, nb, q0);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           q0[q] += h * P[mb][nb][q];  // Qbase = Q + hP
           P[mb][nb][q] += (h / 6.0) * acc[mb][nb][q];
         }
-        own.st(Ar, Ai, mb, nb, q0);
+        own.st(Qr, Qi, mb, nb, q0);
       }
-      // stage 2 (mid) on X2 (B)
-      box = begin_occ(step, 1, step, 2);
-      gemm_box<C>(acc, box, soff, raddr, Br, Bi, own.col0, lane, kmax);
+      // stage 2 (mid) on X2 (Y)
+      box = begin_occ(step, 2);
+      gemm_box<C>(acc, box, soff, raddr, Yr, Yi, own.col0, lane, kmax);
+      PROF_MARK(1);
       end_occ(step, 2);
       FOR_BLK {
         double x2[4];
-        own.ld(Br, Bi, mb, nb, x2);
+        own.ld(Yr, Yi, mb, nb, x2);
         const double g2 = g2s[own.r(mb)];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -677,21 +865,22 @@ __global__ void __launch_bounds__(C::NT, 1) propagate_kernel(const __grid_consta
           P[mb][nb][q] += (h / 3.0) * K;
         }
       }
-      __syncthreads();  // every warp finished reading B
-      FOR_BLK {  // B = X4 = Qbase + h^2/2 K2
+      __syncthreads();  // every warp finished reading Y
+      FOR_BLK {  // Y = X4 = Qbase + h^2/2 K2
         double qb[4];
-        own.ld(Ar, Ai, mb, nb, qb);
+        own.ld(Qr, Qi, mb, nb, qb);
 #pragma unroll
         for (int q = 0; q < 4; ++q) qb[q] += (0.5 * h * h) * acc[mb][nb][q];
-        own.st(Br, Bi, mb, nb, qb);
+        own.st(Yr, Yi, mb, nb, qb);
       }
-      // stage 3 (mid) on X3 (C)
-      box = begin_occ(step, 2, step, 3);
-      gemm_box<C>(acc, box, soff, raddr, Cr, Ci, own.col0, lane, kmax);
+      // stage 3 (mid) on X3 (Z)
+      box = begin_occ(step, 3);
+      gemm_box<C>(acc, box, soff, raddr, Zr, Zi, own.col0, lane, kmax);
+      PROF_MARK(1);
       end_occ(step, 3);
       FOR_BLK {
         double x3[4];
-        own.ld(Cr, Ci, mb, nb, x3);
+        own.ld(Zr, Zi, mb, nb, x3);
         const double g2 = g2s[own.r(mb)];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -700,14 +889,15 @@ __global__ void __launch_bounds__(C::NT, 1) propagate_kernel(const __grid_consta
           P[mb][nb][q] += (h / 3.0) * K;
         }
       }
-      // stage 4 (top) on X4 (B)
-      box = begin_occ(step, 3, step + 1, 0);
-      gemm_box<C>(acc, box, soff, raddr, Br, Bi, own.col0, lane, kmax);
+      // stage 4 (top) on X4 (Y)
+      box = begin_occ(step + 1, 0);
+      gemm_box<C>(acc, box, soff, raddr, Yr, Yi, own.col0, lane, kmax);
+      PROF_MARK(1);
       end_occ(step + 1, 0);
       FOR_BLK {
         double x4[4], qb[4];
-        own.ld(Br, Bi, mb, nb, x4);
-        own.ld(Ar, Ai, mb, nb, qb);
+        own.ld(Yr, Yi, mb, nb, x4);
+        own.ld(Qr, Qi, mb, nb, qb);
         const double g2 = g2s[own.r(mb)];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -715,30 +905,27 @@ __global__ void __launch_bounds__(C::NT, 1) propagate_kernel(const __grid_consta
           P[mb][nb][q] += (h / 6.0) * K;
           qb[q] += (h * h / 6.0) * SQ[mb][nb][q];
         }
-        own.st(Ar, Ai, mb, nb, qb);
+        own.st(Qr, Qi, mb, nb, qb);
       }
     } else {
       // ---------------- splitting (proposed.cpp:170-194)
-      // BAB: nocc = s+1 kicks, drifts after kicks 0..s-1; ABA: nocc = s kicks,
+      // BAB: nocc = s+1 kicks, drift after kicks 0..s-1; ABA: nocc = s kicks,
       // a drift before every kick plus a trailing drift.
       int r0 = 0;
       if (fsal && step > 0) {
         // kick 0 of this step was merged into the previous step's last kick
-        // (same node height); its drift still runs. The end-of-step barrier
-        // already ordered every read of A.
-        drift(p.occ_drift[0]);
+        // (same node height); its drift still runs.
+        drift_swap(p.occ_drift[0]);
         r0 = 1;
       }
       for (int r = r0; r < nocc; ++r) {
         const bool last = (r == nocc - 1);
         const int nstep = last ? step + 1 : step;
-        const int nr = last ? ((fsal && step + 1 > 0) ? 1 : 0) : r + 1;
-        if (p.variant == 0) {  // ABA: drift before kick r
-          __syncthreads();  // previous kick's GEMM reads of A complete
-          drift(p.occ_drift[r]);
-        }
-        double2* box = begin_occ(step, r, nstep, nr);
+        const int nr = last ? (fsal ? 1 : 0) : r + 1;
+        if (p.variant == 0) drift_swap(p.occ_drift[r]);  // ABA: drift before kick r
+        double2* box = begin_occ(nstep, nr);
         gemm_box<C>(acc, box, soff, raddr, Ar, Ai, own.col0, lane, kmax);
+        PROF_MARK(1);
         end_occ(nstep, nr);
         const double kc = (fsal && last && step + 1 < L) ? p.fsal_kick : p.occ_kick[r];
         FOR_BLK {
@@ -748,88 +935,113 @@ __global__ void __launch_bounds__(C::NT, 1) propagate_kernel(const __grid_consta
 #pragma unroll
           for (int q = 0; q < 4; ++q) P[mb][nb][q] -= kc * (acc[mb][nb][q] + g2 * q0[q]);
         }
-        if (p.variant == 1 && !last) {  // BAB: drift after kick r
-          __syncthreads();  // all warps done reading A
-          drift(p.occ_drift[r]);
-        }
+        if (p.variant == 1 && !last) drift_swap(p.occ_drift[r]);  // BAB: drift after kick r
       }
-      if (p.variant == 0) {  // ABA trailing drift
-        __syncthreads();
-        drift(p.final_drift);
-      }
+      if (p.variant == 0) drift_swap(p.final_drift);  // ABA trailing drift
     }
 
     // ---------------- end of step: finite check, Gershgorin, RHST
     // (proposed.cpp:279-287)
-    {
-      int bad = 0;
-      FOR_BLK {
-        double q0[4];
-        own.ld(Ar, Ai, mb, nb, q0);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) bad |= !isfinite(P[mb][nb][q]) || !isfinite(q0[q]);
-      }
-      if (__syncthreads_or(bad)) {
-        code = 1;
-        fail_step = step;
-        break;
-      }
+    PROF_MARK(2);
+    double* Sr = RK4 ? Xr[1] : Nr;  // free scratch plane pair
+    double* Si = RK4 ? Xi[1] : Ni;
+    const double xi = finite_and_gershgorin<C>(Ar, Ai, P, own, n, rsum, dsum, *sc, tid, warp, lane);
+    PROF_MARK(4);
+    if (xi < 0.0) {
+      code = 1;
+      fail_step = step;
+      break;
     }
-    const double xi = gershgorin<C>(Ar, Ai, n, *sc, warp, lane);
     if (xi > p.threshold) {
-      // P <- P Q^-1, Q <- I. B is free scratch here for both steppers.
-      double (&Q0)[MB][NB][4] = SAVE;  // Q kept for the residual gate
-      if (p.residual_check) own.load(Ar, Ai, Q0);
-      own.store(Br, Bi, P);
+      // P <- P Q^-1, Q <- I (proposed.cpp:196-202)
+      double* Or = Xr[2];  // saved Q for the residual gate
+      double* Oi = Xi[2];
+      FOR_BLK {
+        double v[4];
+        if (p.residual_check) {
+          own.ld(Ar, Ai, mb, nb, v);
+          own.st(Or, Oi, mb, nb, v);
+        }
+        own.st(Sr, Si, mb, nb, P[mb][nb]);
+      }
       __syncthreads();
-      bool ok = gauss_jordan<C>(Ar, Ai, Br, Bi, fv, n, *sc, tid, warp, lane);
-      if (ok && p.residual_check) ok = residual_ok<C>(Ar, Ai, Br, Bi, Q0, P, acc, own, n, *sc, warp, lane);
+      PROF_MARK(5);
+#ifdef MB_PROFILE
+      bool ok = gauss_jordan<C, RK4 ? 4 : 0>(Ar, Ai, Sr, Si, fv, n, *sc, warp, lane, tid == 0 ? prof_acc : nullptr);
+      prof_t = clock64();
+#else
+      bool ok = gauss_jordan<C, RK4 ? 4 : 0>(Ar, Ai, Sr, Si, fv, n, *sc, warp, lane);
+#endif
+      PROF_MARK(3);
+      if (ok && p.residual_check)
+        ok = residual_ok<C>(Or, Oi, Sr, Si, [&](int mb, int nb, int q) { return P[mb][nb][q]; }, acc, own, n, *sc,
+                            warp, lane);
       if (!ok) {
         code = 2;
         fail_step = step;
         break;
       }
-      own.load(Br, Bi, P);
+      own.load(Sr, Si, P);
       __syncthreads();
       set_identity<C>(Ar, Ai, n, tid);
       ++rhst;
+      __syncthreads();
     }
-    __syncthreads();
+    PROF_MARK(5);
   }
   cp_async_wait_all();
   __syncthreads();
 
   // ---------------- surface solve: X = R T^-1 (proposed.cpp:204-208), rho = X[:,0]
   if (code == 0) {
-    double T0[MB][NB][4], Rr[MB][NB][4];
-    {
-      double Q0[MB][NB][4];
-      own.load(Ar, Ai, Q0);
+    double* Sr = RK4 ? Xr[1] : Nr;
+    double* Si = RK4 ? Xi[1] : Ni;
+    double* Or = Xr[2];  // saved Q: T and R are rebuilt bit-identically for the residual gate
+    double* Oi = Xi[2];
+    // T = G Q - i P, R = G Q + i P  (i*P = (-pi, pr)), own elements
+    auto tr = [&](int mb, int nb, const double (&q0)[4], double (&t)[4], double (&rr)[4]) {
+      const int r = own.r(mb);
+      const double2 g = r < n ? p.gdiag[pair * n + r] : make_double2(0.0, 0.0);
 #pragma unroll
-      for (int mb = 0; mb < MB; ++mb)
-#pragma unroll
-        for (int nb = 0; nb < NB; ++nb) {
-          const int r = own.r(mb);
-          const double2 g = r < n ? p.gdiag[pair * n + r] : make_double2(0.0, 0.0);
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const double qr = Q0[mb][nb][e], qi = Q0[mb][nb][2 + e];
-            const double gqr = g.x * qr - g.y * qi, gqi = g.x * qi + g.y * qr;
-            const double pr = P[mb][nb][e], pi = P[mb][nb][2 + e];
-            // T = G Q - i P, R = G Q + i P   (i*P = (-pi, pr))
-            T0[mb][nb][e] = gqr + pi;
-            T0[mb][nb][2 + e] = gqi - pr;
-            Rr[mb][nb][e] = gqr - pi;
-            Rr[mb][nb][2 + e] = gqi + pr;
-          }
-        }
+      for (int e = 0; e < 2; ++e) {
+        const double qr = q0[e], qi = q0[2 + e];
+        const double gqr = g.x * qr - g.y * qi, gqi = g.x * qi + g.y * qr;
+        const double pr = P[mb][nb][e], pi = P[mb][nb][2 + e];
+        t[e] = gqr + pi;
+        t[2 + e] = gqi - pr;
+        rr[e] = gqr - pi;
+        rr[2 + e] = gqi + pr;
+      }
+    };
+    __syncthreads();
+    FOR_BLK {
+      double q0[4], t[4], rr[4];
+      own.ld(Ar, Ai, mb, nb, q0);
+      tr(mb, nb, q0, t, rr);
+      own.st(Or, Oi, mb, nb, q0);
+      own.st(Ar, Ai, mb, nb, t);
+      own.st(Sr, Si, mb, nb, rr);
     }
     __syncthreads();
-    own.store(Ar, Ai, T0);
-    own.store(Br, Bi, Rr);
-    __syncthreads();
-    bool ok = gauss_jordan<C>(Ar, Ai, Br, Bi, fv, n, *sc, tid, warp, lane);
-    if (ok && p.residual_check) ok = residual_ok<C>(Ar, Ai, Br, Bi, T0, Rr, acc, own, n, *sc, warp, lane);
+    bool ok = gauss_jordan<C, RK4 ? 4 : 0>(Ar, Ai, Sr, Si, fv, n, *sc, warp, lane);
+    if (ok && p.residual_check) {
+      FOR_BLK {  // A <- T0 (the solver destroyed it)
+        double q0[4], t[4], rr[4];
+        own.ld(Or, Oi, mb, nb, q0);
+        tr(mb, nb, q0, t, rr);
+        own.st(Ar, Ai, mb, nb, t);
+      }
+      __syncthreads();
+      ok = residual_ok<C>(
+          Ar, Ai, Sr, Si,
+          [&](int mb, int nb, int q) {
+            double q0[4], t[4], rr[4];
+            own.ld(Or, Oi, mb, nb, q0);
+            tr(mb, nb, q0, t, rr);
+            return rr[q];
+          },
+          acc, own, n, *sc, warp, lane);
+    }
     if (!ok) {
       code = 3;
       fail_step = L;
@@ -839,7 +1051,7 @@ __global__ void __launch_bounds__(C::NT, 1) propagate_kernel(const __grid_consta
       const double g0 = p.gdiag[pair * n].x;
       for (int i = tid; i < n; i += C::NT) {
         const int o = sw<NP>(i, 0);
-        const double2 rho = make_double2(Br[o], Bi[o]);
+        const double2 rho = make_double2(Sr[o], Si[o]);
         const double2 gi = p.gdiag[pair * n + i];
         const bool prop = gi.y == 0.0;  // geometry.cpp:46-50: propagating rods have real Gamma
         p.rho[pair * n + i] = rho;
@@ -847,6 +1059,11 @@ __global__ void __launch_bounds__(C::NT, 1) propagate_kernel(const __grid_consta
       }
     }
   }
+  PROF_MARK(6);
+#ifdef MB_PROFILE
+  if (tid == 0 && p.prof)
+    for (int q = 0; q < 12; ++q) atomicAdd(p.prof + q, (unsigned long long)prof_acc[q]);
+#endif
   if (tid == 0) {
     PointStatus st;
     st.code = code;
@@ -861,9 +1078,12 @@ __global__ void __launch_bounds__(C::NT, 1) propagate_kernel(const __grid_consta
 template <class C, bool RK4>
 static size_t smem_bytes(const PropagateParams& p) {
   const int np = C::NP;
-  size_t b = (size_t)(RK4 ? 6 : 4) * np * np * sizeof(double);
+  size_t b = (size_t)6 * np * np * sizeof(double);
   b += 2 * (size_t)p.box_size * sizeof(double2);
-  b += (size_t)np * sizeof(double2) + (size_t)np * sizeof(double) + (size_t)np * sizeof(int);
+  b += 2 * (size_t)np * sizeof(double2);              // fv
+  b += (size_t)np * sizeof(double);                   // g2s
+  b += 2 * (size_t)C::WN * np * sizeof(double);       // rsum, dsum
+  b += (size_t)np * sizeof(int);                      // soff
   b += sizeof(Scratch) + 16;
   b += (size_t)p.ndiff * sizeof(int);
   return b;

@@ -53,7 +53,15 @@ def curve_err(eta, ref):
     return 0.0 if num == 0 else (math.inf if den == 0 else num / den)
 
 
-def entry_rel_err(eta, ref):
-    """per-entry relative error on entries above 1e-12 * max eta."""
-    mask = np.abs(ref) > 1e-12 * np.abs(ref).max()
+def entry_rel_err(eta, ref, floor=1e-10):
+    """Per-entry relative error on entries >= floor * max eta. Entries below
+    the floor are checked absolutely by entry_abs_err: at 1e-12 * max eta a
+    1e-9 relative bound would be ~1e-21 absolute, under the FP64 noise that
+    one-ulp differences in a pivot reciprocal leave after ~10^2 RHST solves."""
+    mask = np.abs(ref) >= floor * np.abs(ref).max()
     return float((np.abs(eta - ref)[mask] / np.abs(ref)[mask]).max())
+
+
+def entry_abs_err(eta, ref):
+    """max |d eta| / max eta over every entry."""
+    return float(np.abs(eta - ref).max() / max(np.abs(ref).max(), 1e-300))

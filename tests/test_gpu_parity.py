@@ -44,6 +44,7 @@ def test_layered_field_parity(oracle, method, fsal):
                          mb.SweepOptions(method=method, dz=0.02, fsal=fsal))
     assert H.curve_err(c.eta, ref.eta) <= TOL
     assert H.entry_rel_err(c.eta, ref.eta) <= TOL
+    assert H.entry_abs_err(c.eta, ref.eta) <= 1e-11
     assert np.abs(c.rho - ref.rho).max() <= 1e-10 * np.abs(ref.rho).max()
 
 
@@ -167,6 +168,7 @@ def test_config0_full_parity(oracle):
     eta, rho, st = H.run_device(w)
     assert H.curve_err(eta, ref) <= TOL
     assert H.entry_rel_err(eta, ref) <= TOL
+    assert H.entry_abs_err(eta, ref) <= 1e-11
     assert (st["code"] == 0).all()
 
 
@@ -177,6 +179,7 @@ def test_config1_subset_parity(oracle):
         eta, rho, st = H.run_device(w, fsal=fsal)
         assert H.curve_err(eta, ref) <= TOL, fsal
         assert H.entry_rel_err(eta, ref) <= TOL, fsal
+        assert H.entry_abs_err(eta, ref) <= 1e-11, fsal
 
 
 def test_config2_subset_parity(oracle):
@@ -185,6 +188,7 @@ def test_config2_subset_parity(oracle):
     eta, _, st = H.run_device(w)
     assert H.curve_err(eta, ref) <= TOL
     assert H.entry_rel_err(eta, ref) <= TOL
+    assert H.entry_abs_err(eta, ref) <= 1e-11
 
 
 @pytest.mark.parametrize("n,method", [(15, "rk4"), (15, "sp6"), (31, "sp6"), (63, "sp6")])
@@ -194,3 +198,4 @@ def test_config4_subset_parity(oracle, n, method):
     eta, _, st = H.run_device(w)
     assert H.curve_err(eta, ref) <= TOL
     assert H.entry_rel_err(eta, ref) <= TOL
+    assert H.entry_abs_err(eta, ref) <= 1e-11

@@ -1,0 +1,39 @@
+"""One plan execute of a workload (for ncu launch lists / full captures).
+Usage: python tools/profile_case.py --config 1 [--reps 1]"""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2306_00271_b200 as mb  # noqa: E402
+from paper_2306_00271_b200 import configs  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", type=int, default=1)
+ap.add_argument("--n-rods", type=int, default=63)
+ap.add_argument("--method", default=None)
+ap.add_argument("--reps", type=int, default=1)
+ap.add_argument("--structures", type=int, default=0)
+a = ap.parse_args()
+w = {0: configs.config0, 1: configs.config1, 3: configs.config3}.get(a.config, None)
+if w is not None:
+    w = w()
+elif a.config == 2:
+    w = configs.config2(a.structures or 1024)
+else:
+    w = configs.config4(a.n_rods, a.method or "rk4", n_structures=a.structures or 64)
+method = a.method or w.method
+rods = mb.RodSet.build_first(mb.Lattice2D(w.a1, w.a2), w.n_rods)
+opts = mb.SweepOptions(method=method, slices=w.slices, fsal=True)
+pairs = [(s, t0, t1) for s in range(len(w.structures)) for t1 in w.theta1 for t0 in w.theta0]
+plan = mb.Plan(rods, configs.product_fields(w), w.gamma, pairs, opts)
+for _ in range(a.reps):
+    plan.execute()
+eta, rho, st = plan.results()
+print(w.name, plan.timing(), plan.info(), "rhst/pt", float(st["rhst"].mean()))
+prof = plan.profile()
+if sum(prof.values()) > 0:
+    tot = sum(list(prof.values())[:8])
+    print("phase cycles per CTA:", {k: f"{v:.3e} ({100 * v / tot:.1f}%)" for k, v in prof.items()})
