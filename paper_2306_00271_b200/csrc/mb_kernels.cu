@@ -613,6 +613,140 @@ __device__ bool gauss_jordan(double* Ar, double* Ai, double* Br, double* Bi, dou
 #undef GJ_MARK
 }
 
+// ---------------------------------------------------------------- blocked,
+// pivot-free Gauss-Jordan for strictly row-diagonally-dominant A (finite
+// Gershgorin estimate). Then A^T is column-diagonally dominant, partial
+// pivoting on A^T (the reference's PartialPivLU, kernels.cpp:66) selects the
+// diagonal at every step and every Schur complement stays dominant, so the
+// pivot sequence is the identity: this computes the same elimination with the
+// bulk of the work as DMMA tiles. Panels of 8 rows of A: T = (A_pp)^-1 by
+// warp 0, then every warp owns whole 8-row blocks of [A; B] and applies
+// X[:, panel] <- X[:, panel] T and X[:, rest] -= X[:, panel] A[panel, rest].
+struct PanelScratch {
+  double rr[8 * 64], ri[8 * 64];  // -A[panel rows][:] with the panel columns zeroed
+  double tr[64], ti[64];          // T = A_pp^-1, row-major [k][n]
+  int fail;
+};
+
+// 8x8 complex tile product: c += A[r0.., k0..k0+7] (swizzled NP plane) x
+// B (8 x ldb plane, swizzled rows 0..7) at columns c0..c0+7
+template <class C>
+__device__ __forceinline__ void tile_k8(double (&c)[4], const double* Ar, const double* Ai, int r0, int k0,
+                                        const double* Br, const double* Bi, int c0, int lane, bool b_small) {
+#pragma unroll
+  for (int kb = 0; kb < 2; ++kb) {
+    const int ao = sw<C::NP>(r0 + (lane >> 2), k0 + kb * 4 + (lane & 3));
+    const double ar = Ar[ao], ai = Ai[ao];
+    const int k = kb * 4 + (lane & 3);
+    const int bo = b_small ? k * 8 + (lane >> 2) : sw<C::NP>(k, c0 + (lane >> 2));
+    const double br = Br[bo], bi = Bi[bo];
+    dmma(c[0], c[1], ar, br);
+    dmma(c[2], c[3], ar, bi);
+    dmma(c[0], c[1], dneg(ai), bi);
+    dmma(c[2], c[3], ai, br);
+  }
+}
+
+template <class C>
+__device__ bool gauss_jordan_dominant(double* Ar, double* Ai, double* Br, double* Bi, int n, PanelScratch& ps,
+                                      int tid, int warp, int lane) {
+  constexpr int NP = C::NP;
+  static_assert(NP <= 64, "panel scratch sized for NP <= 64");
+  const int nbB = (n + 7) >> 3;
+  for (int k0 = 0; k0 < n; k0 += 8) {
+    const int bsz = min(8, n - k0);
+    // (1) -A[panel rows][:] with the panel columns zeroed (rank-8 operand)
+    for (int w = tid; w < 8 * NP; w += C::NT) {
+      const int i = w / NP, c = w % NP;
+      const bool keep = i < bsz && (c < k0 || c >= k0 + 8);
+      const int o = sw<NP>(k0 + i, c);
+      ps.rr[sw<NP>(i, c)] = keep ? -Ar[o] : 0.0;
+      ps.ri[sw<NP>(i, c)] = keep ? -Ai[o] : 0.0;
+    }
+    // (2) warp 0: T = A_pp^-1 (row-operation Gauss-Jordan on [A_pp | I]; the
+    // padded block of a partial panel is the identity)
+    if (warp == 0) {
+      const int col = lane & 15;  // lanes 0..7: A_pp columns, 8..15: identity columns
+      double2 v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (col < 8) {
+          const bool real = i < bsz && col < bsz;
+          const int o = sw<NP>(k0 + i, k0 + col);
+          v[i] = real ? make_double2(Ar[o], Ai[o]) : make_double2(i == col ? 1.0 : 0.0, 0.0);
+        } else {
+          v[i] = make_double2(i == col - 8 ? 1.0 : 0.0, 0.0);
+        }
+      }
+      int bad = 0;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const double2 piv = make_double2(__shfl_sync(0xffffffffu, v[t].x, t), __shfl_sync(0xffffffffu, v[t].y, t));
+        double2 f[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          f[i] = make_double2(__shfl_sync(0xffffffffu, v[i].x, t), __shfl_sync(0xffffffffu, v[i].y, t));
+        const double m2 = piv.x * piv.x + piv.y * piv.y;
+        bad |= !(m2 > 0.0);
+        double r;
+        asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(m2));
+        r = r * fma(-m2, r, 2.0);
+        r = r * fma(-m2, r, 2.0);
+        const double2 inv = make_double2(piv.x * r, -piv.y * r);
+        const double2 vt = cmul(v[t], inv);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (i == t) continue;
+          v[i].x -= f[i].x * vt.x - f[i].y * vt.y;
+          v[i].y -= f[i].x * vt.y + f[i].y * vt.x;
+        }
+        v[t] = vt;
+      }
+      if (lane >= 8 && lane < 16) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          ps.tr[i * 8 + (lane - 8)] = v[i].x;
+          ps.ti[i * 8 + (lane - 8)] = v[i].y;
+        }
+      }
+      if (lane == 0) ps.fail = bad;
+    }
+    __syncthreads();
+    if (ps.fail) return false;
+    // (3)+(4): whole 8-row blocks per warp: A rows >= k0+8 (future panels),
+    // B rows < n
+    const int nbA = (NP - k0 - 8) >> 3;
+    for (int rb = warp; rb < nbA + nbB; rb += C::NW) {
+      const bool isA = rb < nbA;
+      double* Xr = isA ? Ar : Br;
+      double* Xi = isA ? Ai : Bi;
+      const int r0 = isA ? k0 + 8 + 8 * rb : 8 * (rb - nbA);
+      double c[4] = {0.0, 0.0, 0.0, 0.0};
+      tile_k8<C>(c, Xr, Xi, r0, k0, ps.tr, ps.ti, 0, lane, true);  // X_panel T
+      __syncwarp();
+      {
+        const int o = sw<NP>(r0 + (lane >> 2), k0 + 2 * (lane & 3));
+        *reinterpret_cast<double2*>(Xr + o) = make_double2(c[0], c[1]);
+        *reinterpret_cast<double2*>(Xi + o) = make_double2(c[2], c[3]);
+      }
+      __syncwarp();
+      for (int cb = 0; cb < NP / 8; ++cb) {
+        if (cb * 8 == k0) continue;
+        const int c0 = cb * 8;
+        const int o = sw<NP>(r0 + (lane >> 2), c0 + 2 * (lane & 3));
+        const double2 xr = *reinterpret_cast<const double2*>(Xr + o);
+        const double2 xi = *reinterpret_cast<const double2*>(Xi + o);
+        double d[4] = {xr.x, xr.y, xi.x, xi.y};
+        tile_k8<C>(d, Xr, Xi, r0, k0, ps.rr, ps.ri, c0, lane, false);
+        *reinterpret_cast<double2*>(Xr + o) = make_double2(d[0], d[1]);
+        *reinterpret_cast<double2*>(Xi + o) = make_double2(d[2], d[3]);
+      }
+    }
+    __syncthreads();
+  }
+  return true;
+}
+
 // identity on the n x n block, zero elsewhere
 template <class C>
 __device__ void set_identity(double* Xr, double* Xi, int n, int tid) {
@@ -685,7 +819,8 @@ __global__ void __launch_bounds__(C::NT, 1) propagate_kernel(const __grid_consta
   double* dsum = rsum + C::WN * NP;                     // [WN][NP]
   int* soff = reinterpret_cast<int*>(dsum + C::WN * NP);  // [NP]
   Scratch* sc = reinterpret_cast<Scratch*>(soff + NP);
-  int* sboxpos = reinterpret_cast<int*>(sc + 1);  // [ndiff]
+  PanelScratch* ps = reinterpret_cast<PanelScratch*>(sc + 1);
+  int* sboxpos = reinterpret_cast<int*>(ps + 1);  // [ndiff]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = p.n;
@@ -966,12 +1101,19 @@ __global__ void __launch_bounds__(C::NT, 1) propagate_kernel(const __grid_consta
       }
       __syncthreads();
       PROF_MARK(5);
+      // finite estimate = strict row dominance: pivot-free blocked solve
+      // (identical pivot sequence); otherwise partial pivoting
+      bool ok;
+      if (isfinite(xi)) {
+        ok = gauss_jordan_dominant<C>(Ar, Ai, Sr, Si, n, *ps, tid, warp, lane);
+      } else {
 #ifdef MB_PROFILE
-      bool ok = gauss_jordan<C, RK4 ? 4 : 0>(Ar, Ai, Sr, Si, fv, n, *sc, warp, lane, tid == 0 ? prof_acc : nullptr);
-      prof_t = clock64();
+        ok = gauss_jordan<C, RK4 ? 4 : 0>(Ar, Ai, Sr, Si, fv, n, *sc, warp, lane, tid == 0 ? prof_acc : nullptr);
+        prof_t = clock64();
 #else
-      bool ok = gauss_jordan<C, RK4 ? 4 : 0>(Ar, Ai, Sr, Si, fv, n, *sc, warp, lane);
+        ok = gauss_jordan<C, RK4 ? 4 : 0>(Ar, Ai, Sr, Si, fv, n, *sc, warp, lane);
 #endif
+      }
       PROF_MARK(3);
       if (ok && p.residual_check)
         ok = residual_ok<C>(Or, Oi, Sr, Si, [&](int mb, int nb, int q) { return P[mb][nb][q]; }, acc, own, n, *sc,
@@ -1084,7 +1226,7 @@ static size_t smem_bytes(const PropagateParams& p) {
   b += (size_t)np * sizeof(double);                   // g2s
   b += 2 * (size_t)C::WN * np * sizeof(double);       // rsum, dsum
   b += (size_t)np * sizeof(int);                      // soff
-  b += sizeof(Scratch) + 16;
+  b += sizeof(Scratch) + sizeof(PanelScratch) + 16;
   b += (size_t)p.ndiff * sizeof(int);
   return b;
 }
