@@ -1,0 +1,327 @@
+// manybeam_b200.hpp — C++ host mirror of the reference forward-model API over
+// the C-ABI (manybeam_b200.h). Same names, argument meaning and error
+// behaviour as /root/reference/proj/core/include/manybeam/*.hpp for the
+// stepper path, so reference callers (driver.cpp:15-21, tests) switch by
+// changing the namespace:
+//
+//   manybeam::RodSet::build            rods.hpp:23-47      -> mb_rods_build
+//   manybeam::PotentialField::*        potential.hpp:35-61 -> mb_field
+//   manybeam::StepperSpec::by_name     proposed.hpp:23-43  -> mb_stepper_by_name
+//   manybeam::AngleGrid::validated     sweep.hpp:17-24
+//   manybeam::rocking_curve            sweep.hpp:37-38     -> mb_rocking_curve
+//   manybeam::curve_error              curve.hpp:38
+//
+// Errors are rethrown as the reference exception types (types.hpp:20-62);
+// BreakdownError carries the step of the first failing row in row order
+// (sweep.cpp:136-137). Header-only; link against libmanybeam_b200.so.
+#pragma once
+
+#include <array>
+#include <cmath>
+#include <complex>
+#include <limits>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "manybeam_b200.h"
+
+namespace manybeam::b200 {
+
+using Complex = std::complex<double>;
+
+struct Error : std::runtime_error {
+  explicit Error(const std::string& m) : std::runtime_error(m) {}
+};
+struct ConfigError : Error { using Error::Error; };
+struct SolverError : Error { using Error::Error; };
+struct SingularMatrixError : SolverError { using SolverError::SolverError; };
+struct BreakdownError : SolverError {
+  BreakdownError(const std::string& m, std::size_t s) : SolverError(m), step(s) {}
+  std::size_t step;
+};
+struct ConvergenceError : SolverError { using SolverError::SolverError; };
+struct DomainError : SolverError { using SolverError::SolverError; };
+struct CompareError : Error { using Error::Error; };
+struct DeviceError : Error { using Error::Error; };
+
+inline void check(int rc, std::size_t step = 0) {
+  if (rc == MB_OK) return;
+  const std::string msg = mb_last_error();
+  switch (rc) {
+    case MB_ERR_CONFIG: throw ConfigError(msg);
+    case MB_ERR_SINGULAR: throw SingularMatrixError(msg);
+    case MB_ERR_BREAKDOWN: throw BreakdownError(msg, step);
+    case MB_ERR_CONVERGENCE: throw ConvergenceError(msg);
+    case MB_ERR_DOMAIN: throw DomainError(msg);
+    case MB_ERR_CUDA: throw DeviceError(msg);
+    case MB_ERR_ARG: throw std::invalid_argument(msg);
+    default: throw SolverError(msg);
+  }
+}
+
+struct Vec2 {
+  double x = 0, y = 0;
+};
+
+// rods.hpp:10-17
+struct Lattice2D {
+  Vec2 a1, a2;
+};
+
+// rods.hpp:23-47 (+ build_first extension)
+class RodSet {
+ public:
+  static RodSet build(const Lattice2D& lat, double cutoff) { return make(lat, cutoff, 0); }
+  static RodSet build_first(const Lattice2D& lat, int n) { return make(lat, 0.0, n); }
+  int size() const { return n_; }
+  int diff_count() const { return ndiff_; }
+  Vec2 k(int i) const { return Vec2{k_[2 * i], k_[2 * i + 1]}; }
+  std::array<int, 2> m(int i) const { return {m_[2 * i], m_[2 * i + 1]}; }
+  int diff_index(int j, int k) const { return diff_index_[(std::size_t)j * n_ + k]; }
+  mb_rods view() const {
+    return mb_rods{n_, k_.data(), m_.data(), ndiff_, diff_.data(), diff_m_.data(), diff_index_.data()};
+  }
+
+ private:
+  static RodSet make(const Lattice2D& lat, double cutoff, int first_n) {
+    const mb_lattice l{{lat.a1.x, lat.a1.y}, {lat.a2.x, lat.a2.y}};
+    RodSet r;
+    check(mb_rods_build(&l, cutoff, first_n, &r.n_, &r.ndiff_, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0));
+    r.k_.resize(2 * (std::size_t)r.n_);
+    r.m_.resize(2 * (std::size_t)r.n_);
+    r.diff_.resize(2 * (std::size_t)r.ndiff_);
+    r.diff_m_.resize(2 * (std::size_t)r.ndiff_);
+    r.diff_index_.resize((std::size_t)r.n_ * r.n_);
+    check(mb_rods_build(&l, cutoff, first_n, &r.n_, &r.ndiff_, r.k_.data(), r.m_.data(), r.diff_.data(),
+                        r.diff_m_.data(), r.diff_index_.data(), r.n_, r.ndiff_));
+    return r;
+  }
+  int n_ = 0, ndiff_ = 0;
+  std::vector<double> k_, diff_;
+  std::vector<int> m_, diff_m_, diff_index_;
+};
+
+// potential.hpp:17-23
+struct GaussianLayer {
+  double z_center = 0.0, amplitude = 0.0, sigma_xy = 1.0, sigma_z = 1.0, absorption = 0.0;
+};
+
+// potential.hpp:35-61 (+ atoms extension)
+class PotentialField {
+ public:
+  static PotentialField zero(double z_bottom) {
+    PotentialField f;
+    f.f_.kind = MB_FIELD_ZERO;
+    f.f_.z_bottom = z_bottom;
+    return f;
+  }
+  static PotentialField gaussian_layers(double z_bottom, const std::vector<GaussianLayer>& layers) {
+    PotentialField f;
+    f.f_.kind = MB_FIELD_GAUSSIAN_LAYERS;
+    f.f_.z_bottom = z_bottom;
+    for (const GaussianLayer& l : layers)
+      f.d0_.insert(f.d0_.end(), {l.z_center, l.amplitude, l.sigma_xy, l.sigma_z, l.absorption});
+    f.f_.nlayers = (int)layers.size();
+    return f;
+  }
+  // entries: (dm, values per grid point)
+  static PotentialField tabulated(double z_bottom, const std::vector<double>& z_grid,
+                                  const std::vector<std::pair<std::array<int, 2>, std::vector<Complex>>>& entries) {
+    PotentialField f;
+    f.f_.kind = MB_FIELD_TABULATED;
+    f.f_.z_bottom = z_bottom;
+    f.d0_ = z_grid;
+    for (const auto& e : entries) {
+      f.i0_.push_back(e.first[0]);
+      f.i0_.push_back(e.first[1]);
+      if (e.second.size() != z_grid.size()) throw ConfigError("potential: tabulated entry sample count mismatch");
+      for (const Complex& v : e.second) {
+        f.d1_.push_back(v.real());
+        f.d1_.push_back(v.imag());
+      }
+    }
+    f.f_.ngrid = (int)z_grid.size();
+    f.f_.nentries = (int)entries.size();
+    return f;
+  }
+  struct Atom {
+    double x, y, z;
+    int species;
+    double B;
+  };
+  static PotentialField atoms(double z_bottom, const std::vector<Atom>& atoms,
+                              const std::vector<std::array<double, 4>>& ff_a,
+                              const std::vector<std::array<double, 4>>& ff_b, double cell_area, double gamma_L,
+                              double particle_sign, double absorption = 0.1) {
+    PotentialField f;
+    f.f_.kind = MB_FIELD_ATOMS;
+    f.f_.z_bottom = z_bottom;
+    for (const Atom& a : atoms) {
+      f.d0_.insert(f.d0_.end(), {a.x, a.y, a.z});
+      f.i0_.push_back(a.species);
+      f.d1_.push_back(a.B);
+    }
+    for (std::size_t s = 0; s < ff_a.size(); ++s) {
+      f.d2_.insert(f.d2_.end(), ff_a[s].begin(), ff_a[s].end());
+      f.d3_.insert(f.d3_.end(), ff_b[s].begin(), ff_b[s].end());
+    }
+    f.f_.natoms = (int)atoms.size();
+    f.f_.nspecies = (int)ff_a.size();
+    f.f_.cell_area = cell_area;
+    f.f_.gamma_L = gamma_L;
+    f.f_.particle_sign = particle_sign;
+    f.f_.absorption = absorption;
+    return f;
+  }
+  double z_bottom() const { return f_.z_bottom; }
+  // C view; pointers refer to this object's storage
+  mb_field view() const {
+    mb_field v = f_;
+    switch (f_.kind) {
+      case MB_FIELD_GAUSSIAN_LAYERS:
+        v.layers = d0_.data();
+        break;
+      case MB_FIELD_TABULATED:
+        v.z_grid = d0_.data();
+        v.entry_dm = i0_.data();
+        v.entry_values = d1_.data();
+        break;
+      case MB_FIELD_ATOMS:
+        v.atom_xyz = d0_.data();
+        v.atom_species = i0_.data();
+        v.atom_B = d1_.data();
+        v.ff_a = d2_.data();
+        v.ff_b = d3_.data();
+        break;
+      default:
+        break;
+    }
+    return v;
+  }
+
+ private:
+  mb_field f_{};
+  std::vector<double> d0_, d1_, d2_, d3_;
+  std::vector<int> i0_;
+};
+
+// sweep.hpp:17-24, sweep.cpp:18-33
+struct AngleGrid {
+  std::vector<double> theta0, theta1;
+  static AngleGrid validated(std::vector<double> t0, std::vector<double> t1) {
+    if (t0.empty()) throw ConfigError("angle grid: theta0 list is empty");
+    if (t1.empty()) throw ConfigError("angle grid: theta1 list is empty");
+    for (double t : t0)
+      if (!(t > 0.0 && t < 90.0)) throw ConfigError("angle grid: glancing angles must lie in (0, 90) degrees");
+    for (std::size_t i = 1; i < t0.size(); ++i)
+      if (!(t0[i] > t0[i - 1])) throw ConfigError("angle grid: theta0 must be strictly increasing");
+    for (double t : t1)
+      if (!std::isfinite(t)) throw ConfigError("angle grid: theta1 must be finite");
+    return AngleGrid{std::move(t0), std::move(t1)};
+  }
+  long rows() const { return (long)(theta0.size() * theta1.size()); }
+};
+
+// sweep.hpp:26-32 for the stepper methods
+struct SweepOptions {
+  std::string method = "rk4";  // rk4 | sp4 | sp6 (conventional is not a device method)
+  double dz = 0.01;
+  long slices = 0;  // EXTENSION: fixed slice count
+  double rhst_threshold = 1000.0;
+  bool residual_check = true;
+  bool fsal = false;
+  int device = 0;
+};
+
+// curve.hpp:19-31
+struct RockingCurve {
+  std::vector<double> theta0, theta1;
+  std::vector<double> eta;  // rows x rods, row-major
+  std::vector<Complex> rho;
+  std::vector<mb_point_status> status;
+  int rods = 0;
+  std::string method;
+  double dz = 0.0, rhst_threshold = 0.0;
+  long rows() const { return (long)theta0.size(); }
+  double eta_at(long r, int i) const { return eta[(std::size_t)r * rods + i]; }
+};
+
+// one device context per process and device, created on first use
+inline mb_context* context(int device) {
+  struct Holder {
+    mb_context* c = nullptr;
+    ~Holder() {
+      if (c) mb_context_destroy(c);
+    }
+  };
+  static thread_local std::vector<std::unique_ptr<Holder>> ctx;
+  if ((int)ctx.size() <= device) ctx.resize((std::size_t)device + 1);
+  if (!ctx[(std::size_t)device]) {
+    auto h = std::make_unique<Holder>();
+    check(mb_context_create(device, &h->c));
+    ctx[(std::size_t)device] = std::move(h);
+  }
+  return ctx[(std::size_t)device]->c;
+}
+
+// sweep.hpp:37-38
+inline RockingCurve rocking_curve(const PotentialField& field, const RodSet& rods, double gamma,
+                                  const AngleGrid& grid, const SweepOptions& opts) {
+  mb_stepper st{};
+  check(mb_stepper_by_name(opts.method.c_str(), &st));
+  const mb_options o{opts.dz, opts.slices, opts.rhst_threshold, opts.residual_check ? 1 : 0, opts.fsal ? 1 : 0};
+  RockingCurve c;
+  c.rods = rods.size();
+  const long rows = grid.rows();
+  c.eta.assign((std::size_t)rows * c.rods, 0.0);
+  c.rho.assign((std::size_t)rows * c.rods, Complex(0.0, 0.0));
+  c.status.assign((std::size_t)rows, mb_point_status{});
+  for (double t1 : grid.theta1)
+    for (double t0 : grid.theta0) {
+      c.theta0.push_back(t0);
+      c.theta1.push_back(t1);
+    }
+  c.method = opts.method;
+  c.dz = opts.dz;
+  c.rhst_threshold = opts.rhst_threshold;
+  const mb_field f = field.view();
+  const mb_rods r = rods.view();
+  const int rc = mb_rocking_curve(context(opts.device), &f, &r, gamma, grid.theta0.data(), (int)grid.theta0.size(),
+                                  grid.theta1.data(), (int)grid.theta1.size(), &st, &o, c.eta.data(),
+                                  reinterpret_cast<double*>(c.rho.data()), c.status.data());
+  std::size_t step = 0;
+  for (const mb_point_status& s : c.status)
+    if (s.code != MB_POINT_OK) {
+      step = (std::size_t)s.step;
+      break;
+    }
+  check(rc, step);
+  return c;
+}
+
+// curve.cpp:22-41
+inline double curve_error(const RockingCurve& cand, const RockingCurve& ref) {
+  if (cand.rows() != ref.rows()) throw CompareError("curve_error: row count mismatch");
+  if (cand.rods != ref.rods) throw CompareError("curve_error: rod count mismatch");
+  for (long r = 0; r < cand.rows(); ++r)
+    if (std::abs(cand.theta0[r] - ref.theta0[r]) > 1e-12 || std::abs(cand.theta1[r] - ref.theta1[r]) > 1e-12)
+      throw CompareError("curve_error: angle grids differ");
+  double num = 0.0, den = 0.0;
+  for (long r = 0; r < cand.rows(); ++r) {
+    double sn = 0.0, sd = 0.0;
+    for (int i = 0; i < cand.rods; ++i) {
+      const double d = cand.eta_at(r, i) - ref.eta_at(r, i);
+      sn += d * d;
+      sd += ref.eta_at(r, i) * ref.eta_at(r, i);
+    }
+    num = std::max(num, std::sqrt(sn));
+    den = std::max(den, std::sqrt(sd));
+  }
+  if (num == 0.0) return 0.0;
+  if (den == 0.0) return std::numeric_limits<double>::infinity();
+  return num / den;
+}
+
+}  // namespace manybeam::b200
