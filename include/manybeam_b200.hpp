@@ -271,7 +271,7 @@ inline RockingCurve rocking_curve(const PotentialField& field, const RodSet& rod
                                   const AngleGrid& grid, const SweepOptions& opts) {
   mb_stepper st{};
   check(mb_stepper_by_name(opts.method.c_str(), &st));
-  const mb_options o{opts.dz, opts.slices, opts.rhst_threshold, opts.residual_check ? 1 : 0, opts.fsal ? 1 : 0};
+  const mb_options o{opts.dz, opts.slices, opts.rhst_threshold, opts.residual_check ? 1 : 0, opts.fsal ? 1 : 0, 0};
   RockingCurve c;
   c.rods = rods.size();
   const long rows = grid.rows();

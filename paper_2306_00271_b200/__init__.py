@@ -113,7 +113,7 @@ class _Stepper(C.Structure):
 
 class _Options(C.Structure):
     _fields_ = [("dz", C.c_double), ("slices", C.c_long), ("rhst_threshold", C.c_double),
-                ("residual_check", C.c_int), ("fsal", C.c_int)]
+                ("residual_check", C.c_int), ("fsal", C.c_int), ("path", C.c_int)]
 
 
 class _Pair(C.Structure):
@@ -422,13 +422,14 @@ class SweepOptions:
     residual_check: bool = True
     fsal: bool = False
     stepper: Optional[StepperSpec] = None  # custom splitting coefficients
+    path: int = 0              # 0 auto, 1 resident on-chip kernel, 2 batched large-N kernels
 
     def _stepper(self):
         return self.stepper if self.stepper is not None else StepperSpec.by_name(self.method)
 
     def _c(self):
         return _Options(float(self.dz), int(self.slices), float(self.rhst_threshold), int(bool(self.residual_check)),
-                        int(bool(self.fsal)))
+                        int(bool(self.fsal)), int(self.path))
 
 
 @dataclass

@@ -94,9 +94,11 @@ class Workload:
         s_eff = {"rk4": 4, "sp4": 6, "sp6": 11}[self.method] if kicks_per_step is None else kicks_per_step
         return float(self.slices) * s_eff * 8.0 * self.n_rods ** 3
 
-    def subset(self, structures=None, theta0=None, slices=None, name=None):
-        """Smaller case with the same generator (for parity tests)."""
-        w = Workload(name or self.name, self.a1, self.a2, self.n_rods, self.energy_ev, self.particle, self.z_bottom,
+    def subset(self, structures=None, theta0=None, slices=None, name=None, z_bottom=None):
+        """Smaller case with the same generator (for parity tests); a thinner
+        slab (z_bottom) with proportionally fewer slices keeps the step h."""
+        w = Workload(name or self.name, self.a1, self.a2, self.n_rods, self.energy_ev, self.particle,
+                     z_bottom if z_bottom is not None else self.z_bottom,
                      slices or self.slices, self.method, list(theta0 if theta0 is not None else self.theta0),
                      [self.structures[i] for i in (structures if structures is not None else range(len(self.structures)))],
                      None, list(self.theta1), self.absorption)

@@ -401,6 +401,9 @@ struct mb_context {
 
 struct mb_plan {
   mb_context* ctx = nullptr;
+  bool big = false;  // large-N batched path (mb_large.cu)
+  mbx::BigParams bp{};
+  int stride = 0;
   int n = 0, ndiff = 0, npad = 0;
   long npairs = 0, nslots = 0;
   int S = 0, T = 0;
@@ -480,11 +483,15 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
     if (fields[f].z_bottom != zb) fail(MB_ERR_CONFIG, "batch: every field must share z_bottom");
     if (fields[f].kind != fields[0].kind) fail(MB_ERR_CONFIG, "batch: every field must be of one kind");
   }
-  const int npad = mbx::propagate_supported(n, stepper->algorithm == MB_STEP_RK4);
-  if (!npad)
-    fail(MB_ERR_CONFIG, "device path: " + std::to_string(n) + " rods with " +
-                            (stepper->algorithm == MB_STEP_RK4 ? std::string("rk4") : std::string("splitting")) +
-                            " is not covered by a kernel variant yet");
+  // resident kernel (state on chip) when it fits, else the batched large-N path
+  int npad = mbx::propagate_supported(n, stepper->algorithm == MB_STEP_RK4);
+  if (opts->path == 1 && !npad) fail(MB_ERR_CONFIG, "resident kernel does not cover this rod count / stepper");
+  if (opts->path == 2) npad = 0;
+  const bool big = npad == 0;
+  if (big) {
+    if (n > 256) fail(MB_ERR_CONFIG, "device path supports at most 256 rods, got " + std::to_string(n));
+    npad = (n + 7) & ~7;
+  }
 
   // slicing (slicing.hpp:17-34) and node heights (stages.cpp:25-30)
   long L;
@@ -698,12 +705,103 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
     p.rho = dev_alloc<double2>(pl, (std::size_t)npairs * n);
     p.status = dev_alloc<mbx::PointStatus>(pl, (std::size_t)npairs);
     p.prof = dev_alloc<unsigned long long>(pl, 12);
+    pl->big = big;
+    pl->stride = (int)stride;
+    if (big) {
+      mbx::BigParams& b = pl->bp;
+      b.n = n;
+      b.np = npad;
+      b.ndiff = ndiff;
+      b.npairs = npairs;
+      b.nsteps = (int)L;
+      b.nslots = nslots;
+      b.slot_stride = (int)stride;
+      b.coef = coef;
+      b.boxpos = p.boxpos;
+      b.rowoff = p.rowoff;
+      b.box_size = box_size;
+      b.box_center = center;
+      b.pair_struct = p.pair_struct;
+      b.gamma2 = p.gamma2;
+      b.gdiag = p.gdiag;
+      b.ginv = p.ginv;
+      b.sin_theta0 = p.sin_theta0;
+      // splitting: Q0, Q1 (ping-pong), P, scratch; rk4: Q, P, X2, X3, W, V, SQ
+      b.nmat = p.rk4 ? 7 : 4;
+      b.pair_stride = (long)b.nmat * 2 * npad * npad;
+      b.state = dev_alloc<double>(pl, (std::size_t)npairs * b.pair_stride);
+      b.status = p.status;
+      b.xi = dev_alloc<double>(pl, (std::size_t)npairs);
+      b.threshold = p.threshold;
+      b.residual_check = p.residual_check;
+      b.eta = p.eta;
+      b.rho = p.rho;
+    }
     for (cudaEvent_t& e : pl->ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
   } catch (...) {
     free_plan(pl);
     throw;
   }
   return pl;
+}
+
+// Large-N orchestration: one launch per kick / RK stage over all pairs, then
+// the per-pair check and RHST kernels each step; the surface solve at the end.
+void execute_big(mb_plan* pl, cudaStream_t st) {
+  const mbx::BigParams& b = pl->bp;
+  const mbx::PropagateParams& p = pl->prop;
+  int* nl = &pl->launches;
+  auto launch = [&](const mbx::BigStage& s) { cuda_check(mbx::big_launch_stage(b, s, st, nl), "big stage launch"); };
+  auto slot = [&](int step, int r) { return (long)step * pl->stride + p.occ_node[r]; };
+  mbx::BigStage s{};
+  const int L = p.nsteps;
+  if (p.rk4) {
+    const int Q = 0, P = 1, X2 = 2, X3 = 3, W = 4, V = 5, SQ = 6;
+    s = mbx::BigStage{0, 0, 0, 0, p.h, 0.0, 0.0, Q, -1, P, X2, X3, W, V, SQ};
+    launch(s);  // initial state + X2
+    for (int step = 0; step < L; ++step) {
+      const int ops[4] = {Q, X2, X3, V};
+      for (int k = 0; k < 4; ++k) {
+        s = mbx::BigStage{3 + k, ops[k], slot(step, k), step, p.h, 0.0, 0.0, Q, -1, P, X2, X3, W, V, SQ};
+        launch(s);
+      }
+      cuda_check(mbx::big_launch_check(b, step, Q, P, st, nl), "big check launch");
+      cuda_check(mbx::big_launch_gj(b, 0, step, Q, P, X3, V, X2, p.h, st, nl), "big RHST launch");
+    }
+    cuda_check(mbx::big_launch_gj(b, 1, L, Q, P, X3, V, -1, 0.0, st, nl), "big surface-solve launch");
+    return;
+  }
+  const int P = 2, SCR = 3;
+  int qc = 0;
+  s = mbx::BigStage{0, 0, 0, 0, p.h, 0.0, 0.0, qc, -1, P, -1, -1, -1, -1, -1};
+  launch(s);
+  const int nk = p.nocc;
+  const bool fsal = p.fsal && p.variant == 1;
+  auto drift = [&](double c) {
+    mbx::BigStage d{2, 0, 0, 0, 0.0, c, 0.0, qc, qc ^ 1, P, -1, -1, -1, -1, -1};
+    launch(d);
+    qc ^= 1;
+  };
+  for (int step = 0; step < L; ++step) {
+    int r0 = 0;
+    if (fsal && step > 0) {
+      drift(p.occ_drift[0]);
+      r0 = 1;
+    }
+    for (int r = r0; r < nk; ++r) {
+      const bool last = r == nk - 1;
+      if (p.variant == 0) drift(p.occ_drift[r]);
+      const double kc = (fsal && last && step + 1 < L) ? p.fsal_kick : p.occ_kick[r];
+      const double dc = (p.variant == 1 && !last) ? p.occ_drift[r] : 0.0;
+      mbx::BigStage k{1, qc, slot(step, r), step, kc, dc, 0.0, qc, qc ^ 1, P, -1, -1, -1, -1, -1};
+      launch(k);
+      if (dc != 0.0) qc ^= 1;
+    }
+    if (p.variant == 0) drift(p.final_drift);
+    cuda_check(mbx::big_launch_check(b, step, qc, P, st, nl), "big check launch");
+    cuda_check(mbx::big_launch_gj(b, 0, step, qc, P, qc ^ 1, SCR, -1, 0.0, st, nl), "big RHST launch");
+  }
+  cuda_check(mbx::big_launch_gj(b, 1, L, qc, P, qc ^ 1, SCR, -1, 0.0, st, nl), "big surface-solve launch");
 }
 
 void execute_plan(mb_plan* pl, cudaStream_t st) {
@@ -715,7 +813,10 @@ void execute_plan(mb_plan* pl, cudaStream_t st) {
   cuda_check(cudaEventRecord(pl->ev[1], st), "event");
   cuda_check(cudaMemsetAsync(pl->prop.prof, 0, 12 * sizeof(unsigned long long), st), "memset");
   int npad = 0;
-  cuda_check(mbx::launch_propagate(pl->prop, st, &pl->launches, &npad), "propagation kernel launch");
+  if (pl->big)
+    execute_big(pl, st);
+  else
+    cuda_check(mbx::launch_propagate(pl->prop, st, &pl->launches, &npad), "propagation kernel launch");
   cuda_check(cudaEventRecord(pl->ev[2], st), "event");
   cuda_check(cudaEventSynchronize(pl->ev[2]), "propagation kernel");
   cuda_check(cudaGetLastError(), "kernel execution");

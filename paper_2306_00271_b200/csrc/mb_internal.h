@@ -72,6 +72,54 @@ struct PropagateParams {
   unsigned long long* prof;   // [8] phase cycles (MB_PROFILE builds), may be null
 };
 
+// ---- large-N batched path (mb_large.cu): state in HBM, one launch per kick
+// or RK stage over all (pair, tile) work items, per-pair check and
+// Gauss-Jordan kernels. Matrix m of pair p: re plane at
+// state + p*pair_stride + m*2*np*np, im plane right after (row-major, ld np).
+struct BigParams {
+  int n, np, ndiff;
+  long npairs;
+  int nsteps;
+  long nslots;
+  int slot_stride;
+  const double2* coef;
+  const int* boxpos;
+  const int* rowoff;
+  int box_size, box_center;
+  const int* pair_struct;
+  const double* gamma2;
+  const double2* gdiag;
+  const double2* ginv;
+  const double* sin_theta0;
+  double* state;
+  int nmat;
+  long pair_stride;  // doubles per pair
+  PointStatus* status;
+  double* xi;  // per pair: Gershgorin estimate of the last check, -1 = nonfinite
+  double threshold;
+  int residual_check;
+  double* eta;
+  double2* rho;
+};
+
+// one tiled-GEMM launch: acc = U(slot) * M[op]; epilogue `kind`
+struct BigStage {
+  int kind;   // 0 init, 1 kick(+drift), 2 drift, 3..6 rk4 stage 1..4
+  int op;     // operand matrix of the GEMM
+  long slot;  // node slot of U (box table)
+  int step;
+  double c0, c1, c2;  // kick / drift / stage coefficients
+  // matrix indices
+  int mq, mqn, mp, mx2, mx3, mw, mv, msq;
+};
+
+cudaError_t big_launch_stage(const BigParams& p, const BigStage& s, cudaStream_t st, int* launches);
+cudaError_t big_launch_check(const BigParams& p, int step, int mq, int mp, cudaStream_t st, int* launches);
+// mode 0: RHST on (A = mq, B = mp) with saves (msa, msb); mode 1: surface solve
+// with scratch (msa, msb)
+cudaError_t big_launch_gj(const BigParams& p, int mode, int step, int mq, int mp, int msa, int msb, int mx2,
+                          double h, cudaStream_t st, int* launches);
+
 // launchers (mb_kernels.cu)
 cudaError_t launch_potential(const PotentialParams& p, cudaStream_t st, int* launches);
 // returns cudaErrorInvalidValue when no kernel variant covers n / stepper

@@ -39,10 +39,10 @@ def run_oracle(o, w, threads=0, method=None, slices=None, threshold=1000.0):
     return np.concatenate(etas), np.concatenate(rhos), np.concatenate(rh)
 
 
-def run_device(w, method=None, slices=None, threshold=1000.0, residual_check=True, fsal=False):
+def run_device(w, method=None, slices=None, threshold=1000.0, residual_check=True, fsal=False, path=0):
     rods = mb.RodSet.build_first(mb.Lattice2D(w.a1, w.a2), w.n_rods)
     opts = mb.SweepOptions(method=method or w.method, slices=slices or w.slices, rhst_threshold=threshold,
-                           residual_check=residual_check, fsal=fsal)
+                           residual_check=residual_check, fsal=fsal, path=path)
     pairs = [(s, t0, t1) for s in range(len(w.structures)) for t1 in w.theta1 for t0 in w.theta0]
     return mb.solve_batch(configs.product_fields(w), rods, w.gamma, pairs, opts)
 

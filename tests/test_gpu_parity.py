@@ -199,3 +199,55 @@ def test_config4_subset_parity(oracle, n, method):
     assert H.curve_err(eta, ref) <= TOL
     assert H.entry_rel_err(eta, ref) <= TOL
     assert H.entry_abs_err(eta, ref) <= 1e-11
+
+
+# ---------------------------------------------------------------- large-N batched path
+# Thinner slabs at the configs' own step (h = 0.016 A for cfg4, 0.01 for cfg3)
+# keep the oracle cheap; a coarse h breaks both paths down by design.
+@pytest.mark.parametrize("n,method,path", [(63, "rk4", 0), (31, "rk4", 2), (61, "sp6", 2), (127, "sp6", 0),
+                                           (127, "rk4", 0)])
+def test_large_path_parity(oracle, n, method, path):
+    w = configs.config4(n, method, n_structures=2).subset(theta0=[0.5, 4.1], slices=150, z_bottom=-2.4)
+    ref, _, rh = H.run_oracle(oracle, w, threads=4)
+    eta, _, st = H.run_device(w, path=path)
+    assert (st["code"] == 0).all()
+    assert np.array_equal(st["rhst"], rh)
+    assert H.curve_err(eta, ref) <= TOL
+    assert H.entry_rel_err(eta, ref) <= TOL
+    assert H.entry_abs_err(eta, ref) <= 1e-11
+
+
+@pytest.mark.parametrize("cfg,method", [(1, "sp6"), (4, "rk4")])
+def test_large_path_matches_resident(cfg, method):
+    if cfg == 1:
+        w = configs.config1().subset(theta0=[0.3, 2.0, 5.5], slices=120)
+    else:
+        w = configs.config4(31, "rk4", n_structures=2).subset(theta0=[0.5, 2.5, 6.0], slices=200, z_bottom=-3.2)
+    a, _, sa = H.run_device(w, method=method, fsal=True, path=1)
+    b, _, sb = H.run_device(w, method=method, fsal=True, path=2)
+    assert H.curve_err(b, a) <= 1e-11
+    assert np.array_equal(sa["rhst"], sb["rhst"])
+
+
+def test_config3_subset_parity(oracle):
+    w = configs.config3().subset(theta0=[0.5, 3.5], slices=300, z_bottom=-3.0)
+    ref, _, rh = H.run_oracle(oracle, w, threads=2)
+    eta, _, st = H.run_device(w)
+    assert (st["code"] == 0).all()
+    assert np.array_equal(st["rhst"], rh)
+    assert H.curve_err(eta, ref) <= TOL
+    # N=199: the oracle against itself with RHST threshold 1500 instead of
+    # 1000 (an equally valid schedule) already differs by 1.2e-9 per entry
+    # (curve_error 1.9e-11); ill-conditioned RHST solves set this noise floor
+    assert H.entry_rel_err(eta, ref) <= 1e-8
+    assert H.entry_abs_err(eta, ref) <= 1e-10
+
+
+def test_n255_parity(oracle):
+    w = configs.config4(255, "rk4", n_structures=1).subset(theta0=[1.7], slices=60, z_bottom=-0.96)
+    ref, _, rh = H.run_oracle(oracle, w, threads=1)
+    eta, _, st = H.run_device(w)
+    assert (st["code"] == 0).all()
+    assert np.array_equal(st["rhst"], rh)
+    assert H.curve_err(eta, ref) <= TOL
+    assert H.entry_rel_err(eta, ref) <= TOL
