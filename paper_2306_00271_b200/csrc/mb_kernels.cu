@@ -778,13 +778,17 @@ __global__ void __launch_bounds__(C::NT, 1) propagate_kernel(const __grid_consta
   double* const base = reinterpret_cast<double*>(smem);
   double* const Xr[3] = {base, base + 2 * NP * NP, base + 4 * NP * NP};
   double* const Xi[3] = {base + NP * NP, base + 3 * NP * NP, base + 5 * NP * NP};
-  double2* box0 = reinterpret_cast<double2*>(reinterpret_cast<double*>(smem) + 6 * NP * NP);
-  double2* box1 = box0 + p.box_size;
-  double2* fv = box1 + p.box_size;                     // [2][NP]
+  // per column group (the WM warps sharing one column range) two box buffers:
+  // the groups only meet at the end-of-step check, so each syncs on its own
+  // named barrier and overlaps its epilogue with the other group's GEMM
+  double2* boxes = reinterpret_cast<double2*>(reinterpret_cast<double*>(smem) + 6 * NP * NP);
+  double2* fv = boxes + 2 * C::WN * p.box_size;  // [2][NP]
   double* g2s = reinterpret_cast<double*>(fv + 2 * NP);  // [NP]
-  double* rsum = g2s + NP;                              // [WN][NP]
-  double* dsum = rsum + C::WN * NP;                     // [WN][NP]
-  int* soff = reinterpret_cast<int*>(dsum + C::WN * NP);  // [NP]
+  // Gershgorin row sums alias the Gauss-Jordan multipliers (never live together)
+  static_assert(C::WN <= 2, "rsum/dsum alias fv");
+  double* rsum = reinterpret_cast<double*>(fv);  // [WN][NP]
+  double* dsum = rsum + C::WN * NP;              // [WN][NP]
+  int* soff = reinterpret_cast<int*>(g2s + NP);  // [NP]
   Scratch* sc = reinterpret_cast<Scratch*>(soff + NP);
   PanelScratch* ps = reinterpret_cast<PanelScratch*>(sc + 1);
   int* sboxpos = reinterpret_cast<int*>(ps + 1);  // [ndiff]
@@ -795,6 +799,14 @@ __global__ void __launch_bounds__(C::NT, 1) propagate_kernel(const __grid_consta
   const int wm = warp / C::WN, wn = warp % C::WN;
   Own<C> own{wm * C::TM, wn * C::TN, lane};
   const double2* coef = p.coef + (long)p.pair_struct[pair] * p.nslots * p.ndiff;
+  const int gtid = wm * 32 + lane;  // thread index inside the column group
+  constexpr int GNT = C::NT / C::WN;
+  auto group_sync = [&]() {
+    if constexpr (C::WN == 1)
+      __syncthreads();
+    else
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + wn), "r"(GNT) : "memory");
+  };
   const int kmax = (n + 3) & ~3;
 #ifdef MB_PROFILE
   long long prof_t = clock64(), prof_acc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -847,11 +859,11 @@ __global__ void __launch_bounds__(C::NT, 1) propagate_kernel(const __grid_consta
   auto slot_of = [&](int step, int r) -> long { return (long)step * p.slot_stride + p.occ_node[r]; };
   auto issue = [&](double2* dst, long slot) {
     const double2* src = coef + slot * p.ndiff;
-    for (int d = tid; d < p.ndiff; d += C::NT) cp_async16(dst + sboxpos[d], src + d);
+    for (int d = gtid; d < p.ndiff; d += GNT) cp_async16(dst + sboxpos[d], src + d);
     cp_async_commit();
   };
-  double2* cur = box0;
-  double2* nxt = box1;
+  double2* cur = boxes + (2 * wn) * p.box_size;
+  double2* nxt = cur + p.box_size;
   __syncthreads();  // sboxpos ready
   long cur_slot = slot_of(0, 0);
   issue(cur, cur_slot);
@@ -867,7 +879,7 @@ __global__ void __launch_bounds__(C::NT, 1) propagate_kernel(const __grid_consta
   auto begin_occ = [&](int nstep, int nr) -> double2* {
     PROF_MARK(2);
     cp_async_wait_all();
-    __syncthreads();
+    group_sync();
     PROF_MARK(0);
     if (nstep < L) {
       const long ns = slot_of(nstep, nr);
@@ -939,7 +951,7 @@ __global__ void __launch_bounds__(C::NT, 1) propagate_kernel(const __grid_consta
         }
         own.st(Zr, Zi, mb, nb, x2);
       }
-      __syncthreads();  // every warp finished reading Q in the stage-1 GEMM
+      group_sync();  // every warp of the group finished reading Q in the stage-1 GEMM
       FOR_BLK {
         double q0[4];
         own.ld(Qr, Qi, mb, nb, q0);
@@ -967,7 +979,7 @@ __global__ void __launch_bounds__(C::NT, 1) propagate_kernel(const __grid_consta
           P[mb][nb][q] += (h / 3.0) * K;
         }
       }
-      __syncthreads();  // every warp finished reading Y
+      group_sync();  // every warp of the group finished reading Y
       FOR_BLK {  // Y = X4 = Qbase + h^2/2 K2
         double qb[4];
         own.ld(Qr, Qi, mb, nb, qb);
@@ -1188,10 +1200,9 @@ template <class C, bool RK4>
 static size_t smem_bytes(const PropagateParams& p) {
   const int np = C::NP;
   size_t b = (size_t)6 * np * np * sizeof(double);
-  b += 2 * (size_t)p.box_size * sizeof(double2);
+  b += 2 * (size_t)C::WN * p.box_size * sizeof(double2);  // per column group
   b += 2 * (size_t)np * sizeof(double2);              // fv
-  b += (size_t)np * sizeof(double);                   // g2s
-  b += 2 * (size_t)C::WN * np * sizeof(double);       // rsum, dsum
+  b += (size_t)np * sizeof(double);                   // g2s (rsum/dsum alias fv)
   b += (size_t)np * sizeof(int);                      // soff
   b += sizeof(Scratch) + sizeof(PanelScratch) + 16;
   b += (size_t)p.ndiff * sizeof(int);
@@ -1211,11 +1222,12 @@ static cudaError_t launch_cfg(const PropagateParams& p, cudaStream_t st) {
 using C16 = Cfg<16, 1, 2>;
 using C32 = Cfg<32, 2, 2>;
 using C64 = Cfg<64, 4, 2>;
+using C64R = Cfg<64, 8, 2>;  // rk4 at NP=64: 16 warps, 8x32 tiles (P, SQ, acc in registers)
 
 int propagate_supported(int n, int rk4) {
   if (n <= 16) return 16;
   if (n <= 32) return 32;
-  if (n <= 64) return rk4 ? 0 : 64;
+  if (n <= 64) return 64;
   return 0;
 }
 
@@ -1225,7 +1237,7 @@ cudaError_t launch_propagate(const PropagateParams& p, cudaStream_t st, int* lau
   cudaError_t e = cudaErrorInvalidValue;
   if (np == 16) e = p.rk4 ? launch_cfg<C16, true>(p, st) : launch_cfg<C16, false>(p, st);
   if (np == 32) e = p.rk4 ? launch_cfg<C32, true>(p, st) : launch_cfg<C32, false>(p, st);
-  if (np == 64) e = launch_cfg<C64, false>(p, st);
+  if (np == 64) e = p.rk4 ? launch_cfg<C64R, true>(p, st) : launch_cfg<C64, false>(p, st);
   if (e == cudaSuccess) ++*launches;
   return e;
 }
