@@ -124,9 +124,9 @@ cudaError_t launch_potential(const PotentialParams& p, cudaStream_t st, int* lau
 // ============================================================== K2
 // Tile configuration: NP = padded rod count; WM x WN warps; each warp owns a
 // (NP/WM) x (NP/WN) complex tile = MB x NB blocks of 8x8 (DMMA C fragments).
-template <int NP_, int WM_, int WN_>
+template <int NP_, int WM_, int WN_, int MINB_ = 1>
 struct Cfg {
-  static constexpr int NP = NP_, WM = WM_, WN = WN_;
+  static constexpr int NP = NP_, WM = WM_, WN = WN_, MINB = MINB_;  // MINB: resident CTAs per SM
   static constexpr int NW = WM * WN, NT = NW * 32;
   static constexpr int TM = NP / WM, TN = NP / WN;
   static constexpr int MB = TM / 8, NB = TN / 8;
@@ -769,7 +769,7 @@ __device__ bool residual_ok(const double* Or, const double* Oi, const double* Xr
 }
 
 template <class C, bool RK4>
-__global__ void __launch_bounds__(C::NT, 1) propagate_kernel(const __grid_constant__ PropagateParams p) {
+__global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_constant__ PropagateParams p) {
   constexpr int NP = C::NP, MB = C::MB, NB = C::NB;
   extern __shared__ __align__(16) unsigned char smem[];
   // planes: splitting uses X0/X1 as ping-pong Q buffers (the free one is the
@@ -1219,8 +1219,13 @@ static cudaError_t launch_cfg(const PropagateParams& p, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// splitting keeps P + acc (+ drift temporaries) in registers: wide tiles, one
+// CTA bound; rk4 (P, SQ, acc) fits 128 registers with narrower tiles and gains
+// resident CTAs per SM
 using C16 = Cfg<16, 1, 2>;
 using C32 = Cfg<32, 2, 2>;
+using C16R = Cfg<16, 2, 2, 4>;  // 4 warps, 8x8 tiles, 4 CTAs/SM
+using C32R = Cfg<32, 4, 2, 2>;  // 8 warps, 8x16 tiles, 2 CTAs/SM
 using C64 = Cfg<64, 4, 2>;
 using C64R = Cfg<64, 8, 2>;  // rk4 at NP=64: 16 warps, 8x32 tiles (P, SQ, acc in registers)
 
@@ -1235,8 +1240,8 @@ cudaError_t launch_propagate(const PropagateParams& p, cudaStream_t st, int* lau
   const int np = propagate_supported(p.n, p.rk4);
   *npad = np;
   cudaError_t e = cudaErrorInvalidValue;
-  if (np == 16) e = p.rk4 ? launch_cfg<C16, true>(p, st) : launch_cfg<C16, false>(p, st);
-  if (np == 32) e = p.rk4 ? launch_cfg<C32, true>(p, st) : launch_cfg<C32, false>(p, st);
+  if (np == 16) e = p.rk4 ? launch_cfg<C16R, true>(p, st) : launch_cfg<C16, false>(p, st);
+  if (np == 32) e = p.rk4 ? launch_cfg<C32R, true>(p, st) : launch_cfg<C32, false>(p, st);
   if (np == 64) e = p.rk4 ? launch_cfg<C64R, true>(p, st) : launch_cfg<C64, false>(p, st);
   if (e == cudaSuccess) ++*launches;
   return e;
