@@ -124,9 +124,10 @@ cudaError_t launch_potential(const PotentialParams& p, cudaStream_t st, int* lau
 // ============================================================== K2
 // Tile configuration: NP = padded rod count; WM x WN warps; each warp owns a
 // (NP/WM) x (NP/WN) complex tile = MB x NB blocks of 8x8 (DMMA C fragments).
-template <int NP_, int WM_, int WN_, int MINB_ = 1>
+template <int NP_, int WM_, int WN_, int MINB_ = 1, bool M3_ = false>
 struct Cfg {
   static constexpr int NP = NP_, WM = WM_, WN = WN_, MINB = MINB_;  // MINB: resident CTAs per SM
+  static constexpr bool M3 = M3_;  // propagation GEMM as 3 real products (see gemm_box)
   static constexpr int NW = WM * WN, NT = NW * 32;
   static constexpr int TM = NP / WM, TN = NP / WN;
   static constexpr int MB = TM / 8, NB = TN / 8;
@@ -225,13 +226,73 @@ __device__ __forceinline__ void cmma(double (&acc)[C::MB][C::NB][4], const doubl
 // acc = U * X, U gathered from the node's box table: U(j,k) = box[raddr_j - off_k]
 // (raddr_j = center + off_j, or -1 for padded rows -> 0). X rows k >= n are zero
 // by construction, so padded columns of U need no mask.
+//
+// C::M3: the complex product as three real DMMA products (the 3M scheme of
+// zgemm3m): T1 = Ur Xr, T2 = Ui Xi, T3 = (Ur+Ui)(Xr+Xi); re = T1 - T2,
+// im = T3 - T1 - T2. 24 instead of 32 DMMAs per 8x8 block-k step; the sums are
+// one DADD per fragment. Normwise error stays O(eps |U| |X|) (Higham, "Stability
+// of a method for multiplying complex matrices with three real matrix
+// multiplications", 1992), which is the bound the propagation needs.
 template <class C>
 __device__ __forceinline__ void gemm_box(double (&acc)[C::MB][C::NB][4], const double2* __restrict__ box,
                                          const int* __restrict__ soff, const int (&raddr)[C::MB],
                                          const double* __restrict__ Xr, const double* __restrict__ Xi,
                                          int col0, int lane, int kmax) {
-  zero<C>(acc);
   const int kl = lane & 3, cl = lane >> 2;
+  if constexpr (C::M3) {
+    double t1[C::MB][C::NB][2], t2[C::MB][C::NB][2], t3[C::MB][C::NB][2];
+#pragma unroll
+    for (int mb = 0; mb < C::MB; ++mb)
+#pragma unroll
+      for (int nb = 0; nb < C::NB; ++nb)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) t1[mb][nb][e] = t2[mb][nb][e] = t3[mb][nb][e] = 0.0;
+#pragma unroll 2
+    for (int k0 = 0; k0 < kmax; k0 += 4) {
+      const int k = k0 + kl;
+      const int offk = soff[k];
+      double ar[C::MB], ai[C::MB], as[C::MB];
+#pragma unroll
+      for (int mb = 0; mb < C::MB; ++mb) {
+        double2 a = make_double2(0.0, 0.0);
+        if (raddr[mb] >= 0) a = box[raddr[mb] - offk];
+        ar[mb] = a.x;
+        ai[mb] = a.y;
+        as[mb] = a.x + a.y;
+      }
+      double br[C::NB], bi[C::NB], bs[C::NB];
+#pragma unroll
+      for (int nb = 0; nb < C::NB; ++nb) {
+        const int o = sw<C::NP>(k, col0 + nb * 8 + cl);
+        br[nb] = Xr[o];
+        bi[nb] = Xi[o];
+        bs[nb] = br[nb] + bi[nb];
+      }
+#pragma unroll
+      for (int mb = 0; mb < C::MB; ++mb)
+#pragma unroll
+        for (int nb = 0; nb < C::NB; ++nb) dmma(t1[mb][nb][0], t1[mb][nb][1], ar[mb], br[nb]);
+#pragma unroll
+      for (int mb = 0; mb < C::MB; ++mb)
+#pragma unroll
+        for (int nb = 0; nb < C::NB; ++nb) dmma(t2[mb][nb][0], t2[mb][nb][1], ai[mb], bi[nb]);
+#pragma unroll
+      for (int mb = 0; mb < C::MB; ++mb)
+#pragma unroll
+        for (int nb = 0; nb < C::NB; ++nb) dmma(t3[mb][nb][0], t3[mb][nb][1], as[mb], bs[nb]);
+    }
+#pragma unroll
+    for (int mb = 0; mb < C::MB; ++mb)
+#pragma unroll
+      for (int nb = 0; nb < C::NB; ++nb)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          acc[mb][nb][e] = t1[mb][nb][e] - t2[mb][nb][e];
+          acc[mb][nb][2 + e] = (t3[mb][nb][e] - t1[mb][nb][e]) - t2[mb][nb][e];
+        }
+    return;
+  }
+  zero<C>(acc);
 #pragma unroll 2
   for (int k0 = 0; k0 < kmax; k0 += 4) {
     const int k = k0 + kl;
@@ -853,7 +914,10 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
   }
 
   double acc[MB][NB][4];
-  double SQ[RK4 ? MB : 1][RK4 ? NB : 1][4];
+  // rk4 K-sum in registers where they allow it (narrow tiles); at NP = 64 the
+  // sum is folded into the Q plane stage by stage instead (stage-2 epilogue)
+  constexpr bool SQR = RK4 && NP <= 32;
+  double SQ[SQR ? MB : 1][SQR ? NB : 1][4];
 
   // table pipeline: slot of occurrence (step, r) = step*stride + node
   auto slot_of = [&](int step, int r) -> long { return (long)step * p.slot_stride + p.occ_node[r]; };
@@ -946,7 +1010,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
         for (int q = 0; q < 4; ++q) {
           const double K = -(acc[mb][nb][q] + g2 * q0[q]);
           acc[mb][nb][q] = K;
-          SQ[mb][nb][q] = K;
+          if constexpr (SQR) SQ[mb][nb][q] = K;
           x2[q] += (0.25 * h * h) * K;  // X3
         }
         own.st(Zr, Zi, mb, nb, x2);
@@ -975,17 +1039,33 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
         for (int q = 0; q < 4; ++q) {
           const double K = -(acc[mb][nb][q] + g2 * x2[q]);
           acc[mb][nb][q] = K;
-          SQ[mb][nb][q] += K;
+          if constexpr (SQR) SQ[mb][nb][q] += K;
           P[mb][nb][q] += (h / 3.0) * K;
         }
       }
       group_sync();  // every warp of the group finished reading Y
-      FOR_BLK {  // Y = X4 = Qbase + h^2/2 K2
+      // Y = X4 = Qbase + h^2/2 K2; Q = Qbase + h^2/6 (K1 + K2), with
+      // h^2/6 K1 = 2/3 (X3 - X2) read back from the planes (no K-sum registers;
+      // the rounding is one ulp of |X3|, the size of the Q update's own)
+      if constexpr (SQR) FOR_BLK {
         double qb[4];
         own.ld(Qr, Qi, mb, nb, qb);
 #pragma unroll
         for (int q = 0; q < 4; ++q) qb[q] += (0.5 * h * h) * acc[mb][nb][q];
         own.st(Yr, Yi, mb, nb, qb);
+      }
+      else FOR_BLK {
+        double qb[4], x2[4], x3[4], x4[4];
+        own.ld(Qr, Qi, mb, nb, qb);
+        own.ld(Yr, Yi, mb, nb, x2);
+        own.ld(Zr, Zi, mb, nb, x3);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          x4[q] = qb[q] + (0.5 * h * h) * acc[mb][nb][q];
+          qb[q] += (h * h / 6.0) * acc[mb][nb][q] + (2.0 / 3.0) * (x3[q] - x2[q]);
+        }
+        own.st(Yr, Yi, mb, nb, x4);
+        own.st(Qr, Qi, mb, nb, qb);
       }
       // stage 3 (mid) on X3 (Z)
       box = begin_occ(step, 3);
@@ -996,11 +1076,23 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
         double x3[4];
         own.ld(Zr, Zi, mb, nb, x3);
         const double g2 = g2s[own.r(mb)];
+        if constexpr (SQR) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const double K = -(acc[mb][nb][q] + g2 * x3[q]);
-          SQ[mb][nb][q] += K;
-          P[mb][nb][q] += (h / 3.0) * K;
+          for (int q = 0; q < 4; ++q) {
+            const double K = -(acc[mb][nb][q] + g2 * x3[q]);
+            SQ[mb][nb][q] += K;
+            P[mb][nb][q] += (h / 3.0) * K;
+          }
+        } else {
+          double qb[4];
+          own.ld(Qr, Qi, mb, nb, qb);  // no GEMM reads Q until the next step
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const double K = -(acc[mb][nb][q] + g2 * x3[q]);
+            qb[q] += (h * h / 6.0) * K;
+            P[mb][nb][q] += (h / 3.0) * K;
+          }
+          own.st(Qr, Qi, mb, nb, qb);
         }
       }
       // stage 4 (top) on X4 (Y)
@@ -1009,17 +1101,18 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
       PROF_MARK(1);
       end_occ(step + 1, 0);
       FOR_BLK {
-        double x4[4], qb[4];
+        double x4[4];
         own.ld(Yr, Yi, mb, nb, x4);
-        own.ld(Qr, Qi, mb, nb, qb);
         const double g2 = g2s[own.r(mb)];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const double K = -(acc[mb][nb][q] + g2 * x4[q]);
-          P[mb][nb][q] += (h / 6.0) * K;
-          qb[q] += (h * h / 6.0) * SQ[mb][nb][q];
+        for (int q = 0; q < 4; ++q) P[mb][nb][q] += (h / 6.0) * -(acc[mb][nb][q] + g2 * x4[q]);
+        if constexpr (SQR) {
+          double qb[4];
+          own.ld(Qr, Qi, mb, nb, qb);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) qb[q] += (h * h / 6.0) * SQ[mb][nb][q];
+          own.st(Qr, Qi, mb, nb, qb);
         }
-        own.st(Qr, Qi, mb, nb, qb);
       }
     } else {
       // ---------------- splitting (proposed.cpp:170-194)
@@ -1220,14 +1313,14 @@ static cudaError_t launch_cfg(const PropagateParams& p, cudaStream_t st) {
 }
 
 // splitting keeps P + acc (+ drift temporaries) in registers: wide tiles, one
-// CTA bound; rk4 (P, SQ, acc) fits 128 registers with narrower tiles and gains
-// resident CTAs per SM
-using C16 = Cfg<16, 1, 2>;
-using C32 = Cfg<32, 2, 2>;
-using C16R = Cfg<16, 2, 2, 4>;  // 4 warps, 8x8 tiles, 4 CTAs/SM
-using C32R = Cfg<32, 4, 2, 2>;  // 8 warps, 8x16 tiles, 2 CTAs/SM
-using C64 = Cfg<64, 4, 2>;
-using C64R = Cfg<64, 8, 2>;  // rk4 at NP=64: 16 warps, 8x32 tiles (P, SQ, acc in registers)
+// CTA bound; rk4 at NP <= 32 (P, SQ, acc) fits 128 registers with narrower
+// tiles and gains resident CTAs per SM; rk4 at NP = 64 runs the splitting
+// tile (C64) with the K-sum folded into the Q plane (16 warps spill)
+using C16 = Cfg<16, 1, 2, 1, true>;
+using C32 = Cfg<32, 2, 2, 1, true>;
+using C16R = Cfg<16, 2, 2, 4, true>;  // 4 warps, 8x8 tiles, 4 CTAs/SM
+using C32R = Cfg<32, 4, 2, 2, true>;  // 8 warps, 8x16 tiles, 2 CTAs/SM
+using C64 = Cfg<64, 4, 2, 1, true>;
 
 int propagate_supported(int n, int rk4) {
   if (n <= 16) return 16;
@@ -1242,7 +1335,7 @@ cudaError_t launch_propagate(const PropagateParams& p, cudaStream_t st, int* lau
   cudaError_t e = cudaErrorInvalidValue;
   if (np == 16) e = p.rk4 ? launch_cfg<C16R, true>(p, st) : launch_cfg<C16, false>(p, st);
   if (np == 32) e = p.rk4 ? launch_cfg<C32R, true>(p, st) : launch_cfg<C32, false>(p, st);
-  if (np == 64) e = p.rk4 ? launch_cfg<C64R, true>(p, st) : launch_cfg<C64, false>(p, st);
+  if (np == 64) e = p.rk4 ? launch_cfg<C64, true>(p, st) : launch_cfg<C64, false>(p, st);
   if (e == cudaSuccess) ++*launches;
   return e;
 }

@@ -76,13 +76,15 @@ __global__ void __launch_bounds__(NTH, 2) big_stage_kernel(const __grid_constant
   };
   stage(0, 0);
 
-  double acc[2][2][4];
+  // 3M complex product (as gemm_box in mb_kernels.cu): T1 = Ur Xr, T2 = Ui Xi,
+  // T3 = (Ur+Ui)(Xr+Xi); re = T1 - T2, im = T3 - T1 - T2.
+  double t1[2][2][2], t2[2][2][2], t3[2][2][2];
 #pragma unroll
   for (int mb = 0; mb < 2; ++mb)
 #pragma unroll
     for (int nb = 0; nb < 2; ++nb)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) acc[mb][nb][q] = 0.0;
+      for (int e = 0; e < 2; ++e) t1[mb][nb][e] = t2[mb][nb][e] = t3[mb][nb][e] = 0.0;
   int raddr[2];
 #pragma unroll
   for (int mb = 0; mb < 2; ++mb) {
@@ -103,41 +105,48 @@ __global__ void __launch_bounds__(NTH, 2) big_stage_kernel(const __grid_constant
         const int kl = kb * 4 + (lane & 3);
         const int k = kc * KC + kl;
         const int offk = k < np ? soff[k] : 0;
-        double ar[2], ai[2], an[2];
+        double ar[2], ai[2], as[2];
 #pragma unroll
         for (int mb = 0; mb < 2; ++mb) {
           double2 a = make_double2(0.0, 0.0);
           if (raddr[mb] >= 0 && k < n) a = box[raddr[mb] - offk];
           ar[mb] = a.x;
           ai[mb] = a.y;
-          an[mb] = dneg(a.y);
+          as[mb] = a.x + a.y;
         }
-        double br[2], bi[2];
+        double br[2], bi[2], bs[2];
 #pragma unroll
         for (int nb = 0; nb < 2; ++nb) {
           const int o = swp(kl, wn * 16 + nb * 8 + (lane >> 2));
           br[nb] = br_[o];
           bi[nb] = bi_[o];
+          bs[nb] = br[nb] + bi[nb];
         }
 #pragma unroll
         for (int mb = 0; mb < 2; ++mb)
 #pragma unroll
-          for (int nb = 0; nb < 2; ++nb) dmma(acc[mb][nb][0], acc[mb][nb][1], ar[mb], br[nb]);
+          for (int nb = 0; nb < 2; ++nb) dmma(t1[mb][nb][0], t1[mb][nb][1], ar[mb], br[nb]);
 #pragma unroll
         for (int mb = 0; mb < 2; ++mb)
 #pragma unroll
-          for (int nb = 0; nb < 2; ++nb) dmma(acc[mb][nb][2], acc[mb][nb][3], ar[mb], bi[nb]);
+          for (int nb = 0; nb < 2; ++nb) dmma(t2[mb][nb][0], t2[mb][nb][1], ai[mb], bi[nb]);
 #pragma unroll
         for (int mb = 0; mb < 2; ++mb)
 #pragma unroll
-          for (int nb = 0; nb < 2; ++nb) dmma(acc[mb][nb][0], acc[mb][nb][1], an[mb], bi[nb]);
-#pragma unroll
-        for (int mb = 0; mb < 2; ++mb)
-#pragma unroll
-          for (int nb = 0; nb < 2; ++nb) dmma(acc[mb][nb][2], acc[mb][nb][3], ai[mb], br[nb]);
+          for (int nb = 0; nb < 2; ++nb) dmma(t3[mb][nb][0], t3[mb][nb][1], as[mb], bs[nb]);
       }
     }
   }
+  double acc[2][2][4];
+#pragma unroll
+  for (int mb = 0; mb < 2; ++mb)
+#pragma unroll
+    for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        acc[mb][nb][e] = t1[mb][nb][e] - t2[mb][nb][e];
+        acc[mb][nb][2 + e] = (t3[mb][nb][e] - t1[mb][nb][e]) - t2[mb][nb][e];
+      }
   if (!warp_live) return;
 
   // ---- fused epilogue on own elements (row r, cols c, c+1)

@@ -4,8 +4,14 @@ import collections
 import csv
 import sys
 
-rows = list(csv.reader(open(sys.argv[1])))
-hdr, data = rows[1], rows[2:]
+rows = list(csv.reader(open(sys.argv[1], errors="replace")))
+hdr = rows[1]
+data = []
+for r in rows[2:]:  # first kernel block only
+    if r and r[0] == "Kernel Name":
+        break
+    if len(r) >= len(hdr) - 1:
+        data.append(r)
 ix = {h: i for i, h in enumerate(hdr)}
 reasons = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
 
