@@ -145,8 +145,9 @@ typedef struct {
   int residual_check;    /* 1: solve_right's 1e-10 residual gate on every RHST (kernels.cpp:75-79) */
   int fsal;              /* 1: merge the last kick of a step with the next step's first
                             (same node height; exact in exact arithmetic). 0 = reference op order */
-  int path;              /* 0 auto, 1 on-chip resident kernel (N <= 64; rk4 N <= 32),
-                            2 batched large-N kernels (state in HBM, N <= 256) */
+  int path;              /* 0 auto, 1 on-chip resident kernel (N <= 64),
+                            2 batched large-N kernels (state in HBM, N <= 256),
+                            3 cluster-resident kernel (64 < N <= 256, one CTA cluster per pair) */
 } mb_options;
 
 /* one (structure, glancing angle) point */

@@ -401,7 +401,8 @@ struct mb_context {
 
 struct mb_plan {
   mb_context* ctx = nullptr;
-  bool big = false;  // large-N batched path (mb_large.cu)
+  bool big = false;      // large-N batched path (mb_large.cu)
+  bool cluster = false;  // cluster-resident path (mb_cluster.cu)
   mbx::BigParams bp{};
   int stride = 0;
   int n = 0, ndiff = 0, npad = 0;
@@ -483,15 +484,15 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
     if (fields[f].z_bottom != zb) fail(MB_ERR_CONFIG, "batch: every field must share z_bottom");
     if (fields[f].kind != fields[0].kind) fail(MB_ERR_CONFIG, "batch: every field must be of one kind");
   }
-  // resident kernel (state on chip) when it fits, else the batched large-N path
+  // resident kernel (state on chip) when it fits; 64 < n <= 256: one cluster
+  // per pair (mb_cluster.cu) when its shared-memory footprint fits, else the
+  // batched large-N path (state in HBM). Final choice after the box size below.
+  if (n > 256) fail(MB_ERR_CONFIG, "device path supports at most 256 rods, got " + std::to_string(n));
   int npad = mbx::propagate_supported(n, stepper->algorithm == MB_STEP_RK4);
   if (opts->path == 1 && !npad) fail(MB_ERR_CONFIG, "resident kernel does not cover this rod count / stepper");
-  if (opts->path == 2) npad = 0;
-  const bool big = npad == 0;
-  if (big) {
-    if (n > 256) fail(MB_ERR_CONFIG, "device path supports at most 256 rods, got " + std::to_string(n));
-    npad = (n + 7) & ~7;
-  }
+  if (opts->path == 2 || opts->path == 3) npad = 0;
+  bool big = npad == 0;
+  if (big) npad = (n + 7) & ~7;
 
   // slicing (slicing.hpp:17-34) and node heights (stages.cpp:25-30)
   long L;
@@ -565,6 +566,26 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
       if (d < 0 || d >= ndiff || boxpos[(std::size_t)d] != center + rowoff[(std::size_t)j] - rowoff[(std::size_t)k])
         fail(MB_ERR_ARG, "rods: diff_index inconsistent with m / diff_m");
     }
+
+  // auto: the cluster kernel keeps the state on chip but spans CS SMs per pair
+  // and serialises its Gauss-Jordan over the cluster; the batched path
+  // amortises its per-pair solves over many pairs. Measured crossover (B200,
+  // round 1): cluster wins for the 61-pair N=199 case, the batched path for
+  // 4096 pairs at N=127/255.
+  bool cluster = false;
+  if (big && (opts->path == 3 || (opts->path == 0 && npairs < 512))) {
+    const int rk4 = stepper->algorithm == MB_STEP_RK4;
+    const size_t need = mbx::cluster_smem_bytes(n, rk4, box_size, ndiff);
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
+    cluster = need > 0 && (optin == 0 || need <= (size_t)optin);
+    if (cluster) {
+      big = false;
+      npad = mbx::cluster_np(n);
+    } else if (opts->path == 3) {
+      fail(MB_ERR_CONFIG, "cluster kernel does not cover this rod count / stepper / box size");
+    }
+  }
 
   mb_plan* pl = new mb_plan();
   pl->ctx = ctx;
@@ -706,7 +727,9 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
     p.status = dev_alloc<mbx::PointStatus>(pl, (std::size_t)npairs);
     p.prof = dev_alloc<unsigned long long>(pl, 12);
     pl->big = big;
+    pl->cluster = cluster;
     pl->stride = (int)stride;
+    if (cluster) p.scratch = dev_alloc<double>(pl, (std::size_t)npairs * 4 * npad * npad);
     if (big) {
       mbx::BigParams& b = pl->bp;
       b.n = n;
@@ -732,6 +755,10 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
       b.state = dev_alloc<double>(pl, (std::size_t)npairs * b.pair_stride);
       b.status = p.status;
       b.xi = dev_alloc<double>(pl, (std::size_t)npairs);
+      b.chk = dev_alloc<double>(pl, (std::size_t)npairs * ((npad + 15) / 16) * 4);
+      b.chk_count = dev_alloc<unsigned>(pl, (std::size_t)npairs);
+      cuda_check(cudaMemsetAsync(b.chk_count, 0, (std::size_t)npairs * sizeof(unsigned), pl->ctx->stream),
+                 "cudaMemsetAsync");
       b.threshold = p.threshold;
       b.residual_check = p.residual_check;
       b.eta = p.eta;
@@ -815,6 +842,8 @@ void execute_plan(mb_plan* pl, cudaStream_t st) {
   int npad = 0;
   if (pl->big)
     execute_big(pl, st);
+  else if (pl->cluster)
+    cuda_check(mbx::launch_cluster(pl->prop, st, &pl->launches), "cluster propagation kernel launch");
   else
     cuda_check(mbx::launch_propagate(pl->prop, st, &pl->launches, &npad), "propagation kernel launch");
   cuda_check(cudaEventRecord(pl->ev[2], st), "event");

@@ -70,6 +70,7 @@ struct PropagateParams {
   double2* rho;               // [npairs][n]
   PointStatus* status;        // [npairs]
   unsigned long long* prof;   // [8] phase cycles (MB_PROFILE builds), may be null
+  double* scratch;            // cluster kernel: per pair 4 NP^2 doubles (RHST / surface solve)
 };
 
 // ---- large-N batched path (mb_large.cu): state in HBM, one launch per kick
@@ -96,6 +97,8 @@ struct BigParams {
   long pair_stride;  // doubles per pair
   PointStatus* status;
   double* xi;  // per pair: Gershgorin estimate of the last check, -1 = nonfinite
+  double* chk;               // [npairs][ceil(np/16)][4] check partials
+  unsigned* chk_count;       // [npairs] arrival counters (zeroed at plan creation)
   double threshold;
   int residual_check;
   double* eta;
@@ -125,5 +128,9 @@ cudaError_t launch_potential(const PotentialParams& p, cudaStream_t st, int* lau
 // returns cudaErrorInvalidValue when no kernel variant covers n / stepper
 cudaError_t launch_propagate(const PropagateParams& p, cudaStream_t st, int* launches, int* npad);
 int propagate_supported(int n, int rk4);  // padded size or 0
+// cluster-resident kernel (mb_cluster.cu) for 64 < n <= 256
+int cluster_np(int n);  // padded row count (128 / 256) or 0
+size_t cluster_smem_bytes(int n, int rk4, int box_size, int ndiff);
+cudaError_t launch_cluster(const PropagateParams& p, cudaStream_t st, int* launches);
 
 }  // namespace mbx

@@ -29,11 +29,19 @@ namespace mbx {
 
 namespace {
 
-constexpr int BM = 64, BN = 32, KC = 32;  // output tile, K chunk
+constexpr int BM = 64, BN = 32, KC = 16;  // output tile, K chunk
 constexpr int NTH = 256;                  // 8 warps: 4 (rows) x 2 (cols), warp tile 16 x 16
 constexpr int NPMAX = 256;
 
 __device__ __forceinline__ int swp(int k, int c) { return k * BN + (c ^ ((k & 3) << 2)); }
+
+__device__ __forceinline__ int epi_sw(int r, int c) { return r * BN + (c ^ ((r & 1) << 3)); }
+
+// byte offset of the epilogue tiles in the stage kernel's dynamic smem
+__host__ __device__ inline size_t epi_offset(const BigParams& p) {
+  const size_t b = 4 * KC * BN * sizeof(double) + (size_t)p.box_size * sizeof(double2) + (size_t)p.np * sizeof(int);
+  return (b + 15) & ~(size_t)15;
+}
 
 __device__ __forceinline__ double* mat(const BigParams& p, long pair, int m) {
   return p.state + pair * p.pair_stride + (long)m * 2 * p.np * p.np;
@@ -46,6 +54,9 @@ __global__ void __launch_bounds__(NTH, 2) big_stage_kernel(const __grid_constant
   double* xp = reinterpret_cast<double*>(smem);                 // [2 buf][2 plane][KC*BN]
   double2* box = reinterpret_cast<double2*>(xp + 4 * KC * BN);  // [box_size]
   int* soff = reinterpret_cast<int*>(box + p.box_size);         // [np]
+  // epilogue operand tiles (X = op, P) prefetched during the last K chunk:
+  // [2 operand][2 plane][BM][BN], rows swizzled by epi_sw
+  double* epi = reinterpret_cast<double*>(smem + epi_offset(p));
 
   const int np = p.np, n = p.n;
   const int tiles_n = (np + BN - 1) / BN, tiles_m = (np + BM - 1) / BM, tiles = tiles_m * tiles_n;
@@ -93,10 +104,25 @@ __global__ void __launch_bounds__(NTH, 2) big_stage_kernel(const __grid_constant
   }
   const bool warp_live = (r0 + wm * 16 < np) && (c0 + wn * 16 < np);
 
+  auto prefetch_epi = [&]() {
+    for (int idx = tid; idx < 4 * BM * (BN / 2); idx += NTH) {
+      const int pl = idx / (BM * (BN / 2)), rem = idx % (BM * (BN / 2));
+      const int r = rem / (BN / 2), c = 2 * (rem % (BN / 2));
+      const int gr = r0 + r, gc = c0 + c;
+      if (gr < np && gc < np) {
+        const double* src = mat(p, pair, (pl >> 1) ? s.mp : s.op) + (long)(pl & 1) * np * np + (long)gr * np + gc;
+        cp_async16(epi + pl * BM * BN + epi_sw(r, c), src);
+      }
+    }
+    cp_async_commit();
+  };
   for (int kc = 0; kc < nck; ++kc) {
     cp_async_wait_all();
     __syncthreads();
-    if (kc + 1 < nck) stage(kc + 1, (kc + 1) & 1);
+    if (kc + 1 < nck)
+      stage(kc + 1, (kc + 1) & 1);
+    else
+      prefetch_epi();
     const double* br_ = xp + ((kc & 1) * 2 + 0) * KC * BN;
     const double* bi_ = xp + ((kc & 1) * 2 + 1) * KC * BN;
     if (warp_live) {
@@ -137,6 +163,8 @@ __global__ void __launch_bounds__(NTH, 2) big_stage_kernel(const __grid_constant
       }
     }
   }
+  cp_async_wait_all();
+  __syncthreads();
   double acc[2][2][4];
 #pragma unroll
   for (int mb = 0; mb < 2; ++mb)
@@ -176,16 +204,32 @@ __global__ void __launch_bounds__(NTH, 2) big_stage_kernel(const __grid_constant
       const int c = c0 + wn * 16 + nb * 8 + 2 * (lane & 3);
       if (c >= np) continue;
       const long o = (long)r * np + c;
+      const int eo = epi_sw(r - r0, c - c0);
       double x[4];
-      ld(s.op, o, x);
+      {
+        const double2 a = *reinterpret_cast<const double2*>(epi + eo);
+        const double2 b = *reinterpret_cast<const double2*>(epi + BM * BN + eo);
+        x[0] = a.x;
+        x[1] = a.y;
+        x[2] = b.x;
+        x[3] = b.y;
+      }
+      double pe[4];
+      {
+        const double2 a = *reinterpret_cast<const double2*>(epi + 2 * BM * BN + eo);
+        const double2 b = *reinterpret_cast<const double2*>(epi + 3 * BM * BN + eo);
+        pe[0] = a.x;
+        pe[1] = a.y;
+        pe[2] = b.x;
+        pe[3] = b.y;
+      }
       double K[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) K[q] = acc[mb][nb][q] + g2 * x[q];  // (U + G^2) X
       if (s.kind == 1) {  // splitting kick: P -= hb (U+G^2) Q ; optional drift Qn = Q + ha P
         double pv[4];
-        ld(s.mp, o, pv);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) pv[q] -= s.c0 * K[q];
+        for (int q = 0; q < 4; ++q) pv[q] = pe[q] - s.c0 * K[q];
         st(s.mp, o, pv);
         if (s.c1 != 0.0) {
           double qn[4];
@@ -199,8 +243,7 @@ __global__ void __launch_bounds__(NTH, 2) big_stage_kernel(const __grid_constant
         const double h = s.c0;
 #pragma unroll
         for (int q = 0; q < 4; ++q) K[q] = -K[q];
-        double pv[4], sq[4], w[4];
-        ld(s.mp, o, pv);
+        double pv[4] = {pe[0], pe[1], pe[2], pe[3]}, sq[4], w[4];
         if (s.kind == 3) {  // X = Q: SQ = K1, X3 = X2 + h^2/4 K1, W = Q + hP, P += h/6 K1
           double x2[4];
           ld(s.mx2, o, x2);
@@ -293,20 +336,28 @@ __global__ void big_elem_kernel(const __grid_constant__ BigParams p, const __gri
 }
 
 // ------------------------------------------------------------------ check
+// One CTA per (pair, 16-row block): finite check of those rows of Q and P and
+// their Gershgorin terms; the last CTA of a pair (arrival counter) reduces the
+// blocks in a fixed order, so the estimate is deterministic.
+constexpr int CHK_ROWS = 16;
 __global__ void __launch_bounds__(NTH) big_check_kernel(const __grid_constant__ BigParams p, int step, int mq,
                                                         int mp) {
   __shared__ double sh[3][NTH / 32];
-  const long pair = blockIdx.x;
-  if (p.status[pair].code != 0) return;
+  __shared__ int last;
   const int np = p.np, n = p.n, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nrb = (np + CHK_ROWS - 1) / CHK_ROWS;
+  const long pair = blockIdx.x / nrb;
+  const int rb = blockIdx.x % nrb;
+  if (p.status[pair].code != 0) return;
   const long NN = (long)np * np;
   const double* Q = mat(p, pair, mq);
   const double* P = mat(p, pair, mp);
+  const int i0 = rb * CHK_ROWS, i1 = min(np, i0 + CHK_ROWS);
   int bad = 0;
-  for (long o = tid; o < NN; o += NTH)
+  for (long o = (long)i0 * np + tid; o < (long)i1 * np; o += NTH)
     bad |= !isfinite(Q[o]) || !isfinite(Q[NN + o]) || !isfinite(P[o]) || !isfinite(P[NN + o]);
   double hi = 0.0, lo = __longlong_as_double(0x7ff0000000000000LL), nd = 0.0;
-  for (int i = warp; i < n; i += NTH / 32) {
+  for (int i = i0 + warp; i < min(i1, n); i += NTH / 32) {
     double rs = 0.0, dg = 0.0;
     for (int j = lane; j < n; j += 32) {
       const long o = (long)i * np + j;
@@ -329,6 +380,7 @@ __global__ void __launch_bounds__(NTH) big_check_kernel(const __grid_constant__ 
     sh[2][warp] = nd;
   }
   __syncthreads();
+  double* part = p.chk + pair * (long)nrb * 4;
   if (tid == 0) {
     double H = 0.0, L = __longlong_as_double(0x7ff0000000000000LL), B = 0.0;
     for (int w = 0; w < NTH / 32; ++w) {
@@ -336,15 +388,34 @@ __global__ void __launch_bounds__(NTH) big_check_kernel(const __grid_constant__ 
       L = fmin(L, sh[1][w]);
       B = fmax(B, sh[2][w]);
     }
-    if (bad) {
-      p.xi[pair] = -1.0;
-      PointStatus st = p.status[pair];
-      st.code = 1;
-      st.step = step;
-      p.status[pair] = st;
-    } else {
-      p.xi[pair] = B > 0.0 ? __longlong_as_double(0x7ff0000000000000LL) : H / L;
-    }
+    part[rb * 4 + 0] = H;
+    part[rb * 4 + 1] = L;
+    part[rb * 4 + 2] = B;
+    part[rb * 4 + 3] = bad ? 1.0 : 0.0;
+    __threadfence();
+    const unsigned done = atomicAdd(p.chk_count + pair, 1u);
+    last = done == (unsigned)(nrb - 1);
+  }
+  __syncthreads();
+  if (!last || tid != 0) return;
+  __threadfence();
+  p.chk_count[pair] = 0u;  // re-armed for the next step's check
+  double H = 0.0, L = __longlong_as_double(0x7ff0000000000000LL), B = 0.0, F = 0.0;
+  const volatile double* vp = part;
+  for (int r = 0; r < nrb; ++r) {
+    H = fmax(H, vp[r * 4 + 0]);
+    L = fmin(L, vp[r * 4 + 1]);
+    B = fmax(B, vp[r * 4 + 2]);
+    F = fmax(F, vp[r * 4 + 3]);
+  }
+  if (F > 0.0) {
+    p.xi[pair] = -1.0;
+    PointStatus st = p.status[pair];
+    st.code = 1;
+    st.step = step;
+    p.status[pair] = st;
+  } else {
+    p.xi[pair] = B > 0.0 ? __longlong_as_double(0x7ff0000000000000LL) : H / L;
   }
 }
 
@@ -698,10 +769,10 @@ cudaError_t big_launch_stage(const BigParams& p, const BigStage& s, cudaStream_t
     big_elem_kernel<<<blocks, 256, 0, st>>>(p, s);
   } else {
     const int tiles = ((p.np + BM - 1) / BM) * ((p.np + BN - 1) / BN);
-    const size_t smem = 4 * KC * BN * sizeof(double) + (size_t)p.box_size * sizeof(double2) + (size_t)p.np * sizeof(int);
+    const size_t smem = epi_offset(p) + 4 * BM * BN * sizeof(double);
     static bool attr = false;
     if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(big_stage_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+      cudaError_t e = cudaFuncSetAttribute(big_stage_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       if (e != cudaSuccess) return e;
       attr = true;
     }
@@ -712,7 +783,8 @@ cudaError_t big_launch_stage(const BigParams& p, const BigStage& s, cudaStream_t
 }
 
 cudaError_t big_launch_check(const BigParams& p, int step, int mq, int mp, cudaStream_t st, int* launches) {
-  big_check_kernel<<<(unsigned)p.npairs, NTH, 0, st>>>(p, step, mq, mp);
+  const int nrb = (p.np + CHK_ROWS - 1) / CHK_ROWS;
+  big_check_kernel<<<(unsigned)(p.npairs * nrb), NTH, 0, st>>>(p, step, mq, mp);
   ++*launches;
   return cudaGetLastError();
 }

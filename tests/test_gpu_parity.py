@@ -204,8 +204,9 @@ def test_config4_subset_parity(oracle, n, method):
 # ---------------------------------------------------------------- large-N batched path
 # Thinner slabs at the configs' own step (h = 0.016 A for cfg4, 0.01 for cfg3)
 # keep the oracle cheap; a coarse h breaks both paths down by design.
-@pytest.mark.parametrize("n,method,path", [(63, "rk4", 0), (31, "rk4", 2), (61, "sp6", 2), (127, "sp6", 0),
-                                           (127, "rk4", 0)])
+@pytest.mark.parametrize("n,method,path", [(63, "rk4", 0), (31, "rk4", 2), (61, "sp6", 2), (127, "sp6", 2),
+                                           (127, "rk4", 2), (127, "sp6", 3), (127, "rk4", 3), (81, "sp6", 3),
+                                           (143, "sp6", 3), (143, "rk4", 2)])
 def test_large_path_parity(oracle, n, method, path):
     w = configs.config4(n, method, n_structures=2).subset(theta0=[0.5, 4.1], slices=150, z_bottom=-2.4)
     ref, _, rh = H.run_oracle(oracle, w, threads=4)
@@ -229,10 +230,11 @@ def test_large_path_matches_resident(cfg, method):
     assert np.array_equal(sa["rhst"], sb["rhst"])
 
 
-def test_config3_subset_parity(oracle):
+@pytest.mark.parametrize("path", [2, 3])
+def test_config3_subset_parity(oracle, path):
     w = configs.config3().subset(theta0=[0.5, 3.5], slices=300, z_bottom=-3.0)
     ref, _, rh = H.run_oracle(oracle, w, threads=2)
-    eta, _, st = H.run_device(w)
+    eta, _, st = H.run_device(w, path=path)
     assert (st["code"] == 0).all()
     assert np.array_equal(st["rhst"], rh)
     assert H.curve_err(eta, ref) <= TOL
@@ -243,11 +245,24 @@ def test_config3_subset_parity(oracle):
     assert H.entry_abs_err(eta, ref) <= 1e-10
 
 
-def test_n255_parity(oracle):
-    w = configs.config4(255, "rk4", n_structures=1).subset(theta0=[1.7], slices=60, z_bottom=-0.96)
+@pytest.mark.parametrize("method,path", [("rk4", 2), ("sp6", 3)])
+def test_n255_parity(oracle, method, path):
+    w = configs.config4(255, method, n_structures=1).subset(theta0=[1.7], slices=60, z_bottom=-0.96)
     ref, _, rh = H.run_oracle(oracle, w, threads=1)
-    eta, _, st = H.run_device(w)
+    eta, _, st = H.run_device(w, path=path)
     assert (st["code"] == 0).all()
     assert np.array_equal(st["rhst"], rh)
     assert H.curve_err(eta, ref) <= TOL
     assert H.entry_rel_err(eta, ref) <= TOL
+
+
+@pytest.mark.parametrize("n,method", [(127, "sp6"), (199, "sp6"), (127, "rk4")])
+def test_cluster_matches_batched(n, method):
+    """Two independent large-N designs (state resident in a CTA cluster vs in
+    HBM) on the same batch; the RHST schedules coincide."""
+    w = configs.config4(n, method, n_structures=2).subset(theta0=[0.5, 2.5, 6.0], slices=200, z_bottom=-3.2)
+    a, _, sa = H.run_device(w, path=3)
+    b, _, sb = H.run_device(w, path=2)
+    assert (sa["code"] == 0).all() and (sb["code"] == 0).all()
+    assert np.array_equal(sa["rhst"], sb["rhst"])
+    assert H.curve_err(a, b) <= 1e-9

@@ -16,6 +16,9 @@ ap.add_argument("--n-rods", type=int, default=63)
 ap.add_argument("--method", default=None)
 ap.add_argument("--reps", type=int, default=1)
 ap.add_argument("--structures", type=int, default=0)
+ap.add_argument("--no-residual", action="store_true")
+ap.add_argument("--angles", type=int, default=0)
+ap.add_argument("--slices", type=int, default=0)
 a = ap.parse_args()
 w = {0: configs.config0, 1: configs.config1, 3: configs.config3}.get(a.config, None)
 if w is not None:
@@ -24,15 +27,17 @@ elif a.config == 2:
     w = configs.config2(a.structures or 1024)
 else:
     w = configs.config4(a.n_rods, a.method or "rk4", n_structures=a.structures or 64)
+if a.angles or a.slices:
+    w = w.subset(theta0=list(w.theta0[:a.angles]) if a.angles else None, slices=a.slices or None)
 method = a.method or w.method
 rods = mb.RodSet.build_first(mb.Lattice2D(w.a1, w.a2), w.n_rods)
-opts = mb.SweepOptions(method=method, slices=w.slices, fsal=True)
+opts = mb.SweepOptions(method=method, slices=w.slices, fsal=True, residual_check=not a.no_residual)
 pairs = [(s, t0, t1) for s in range(len(w.structures)) for t1 in w.theta1 for t0 in w.theta0]
 plan = mb.Plan(rods, configs.product_fields(w), w.gamma, pairs, opts)
 for _ in range(a.reps):
     plan.execute()
 eta, rho, st = plan.results()
-print(w.name, plan.timing(), plan.info(), "rhst/pt", float(st["rhst"].mean()))
+print(w.name, plan.timing(), plan.info(), "rhst/pt", float(st["rhst"].mean()), "pivoting/pt", float(st["reserved"].mean()))
 prof = plan.profile()
 if sum(prof.values()) > 0:
     tot = sum(list(prof.values())[:8])
