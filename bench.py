@@ -107,8 +107,18 @@ def fp64_peak():
         return 37.1, "fallback 37.1 TF/s (own DMMA measurement, round 1)"
 
 
+NCU_SUMMARY = "ncu_summary_r01c.json"  # the latest committed capture of the bench command
+
+
+def hbm_peak():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except Exception:
+        return 6542.7, "fallback: MEASURED_PEAKS.json value of round 1 (6542.7 GB/s)"
+
+
 def ncu_traffic(name):
-    p = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
+    p = os.path.join(ROOT, "profiles", NCU_SUMMARY)
     try:
         return json.load(open(p)).get(name, {}).get("dram_bytes_per_launch")
     except Exception:
@@ -230,6 +240,7 @@ def main():
     rhst_mean = float(status["rhst"].mean())
     plan.close()
 
+    pot_bytes = float(info["coef_bytes"])  # 16 B x structures x slots x ndiff
     ms_step = tot / args.steps
     if dist:
         tt = torch.tensor([ms_step], device="cuda", dtype=torch.float64)
@@ -300,10 +311,17 @@ def main():
                                 if sharded else f"one batch per GPU, {world} rank(s), no collective")},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": ncu_traffic("propagate"),
-                         "kernel": f"propagate_kernel (NP={info['npad']})", "peak_source": peak_src,
+                         "kernel": (f"propagate_kernel (NP={info['npad']})" if w.n_rods <= 64 else f"K2 large-N path (NP={info['npad']})"), "peak_source": peak_src,
                          "flops_per_launch": flops_launch,
                          "flops_rule": f"points * L * {s_eff(method)} * 8 N^3 (N={w.n_rods}; RHST/extraction excluded)",
                          "ms_per_launch": ms_prop},
+            "potential_roofline": {"bound": "hbm", "kernel": "potential_coef_kernel (K1)",
+                                   "achieved": pot_bytes / (pot / args.steps * 1e-3) / 1e9, "unit": "GB/s",
+                                   "peak": hbm_peak()[0], "peak_source": hbm_peak()[1],
+                                   "frac": pot_bytes / (pot / args.steps * 1e-3) / 1e9 / hbm_peak()[0],
+                                   "bytes_per_launch": pot_bytes,
+                                   "bytes_rule": "16 B x structures x node slots x ndiff (coefficient table write)",
+                                   "note": "K1 is ~0.1% of the step; at cfg1 it is bound by its exp() evaluations"},
             "cpu_baseline": cb, "e2e": e2e, "gpu_launches": launches,
             "kernel_ms": {"potential": pot / args.steps, "propagate": ms_prop},
             "rhst_per_point": rhst_mean, "wall_s_timed": t_wall, "clocks": ck,

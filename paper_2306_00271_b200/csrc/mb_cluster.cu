@@ -72,14 +72,8 @@ struct CCfg {
 // halves (B fragments: 4 rows x 8 cols; own-element double2 accesses)
 __device__ __forceinline__ int ss(int r, int c) { return r * SW + (c ^ ((r & 1) << 3)); }
 
-struct GjLocal {
-  int p;
-  double pv;
-  double2 inv;
-};
-
 struct Layout {
-  size_t planes, boxes, fpub, floc, tpub, tloc, wch, scr, gjl, g2s, rsum, dsum, pubv, occ, soff, sboxpos, total;
+  size_t planes, boxes, fpub, tpub, tloc, wch, scr, g2s, rsum, dsum, pubv, occ, soff, sboxpos, total;
 };
 
 __host__ __device__ inline size_t al16(size_t b) { return (b + 15) & ~(size_t)15; }
@@ -93,8 +87,6 @@ __host__ __device__ inline Layout cluster_layout(int np, int nq, int box_size, i
   o += al16((size_t)2 * box_size * sizeof(double2));
   L.fpub = o;
   o += al16((size_t)2 * np * sizeof(double2));
-  L.floc = o;
-  o += al16((size_t)np * sizeof(double2));
   L.tpub = o;  // published panel table: 1/pivot, |pivot|^2, pivot column, flag
   o += al16((size_t)(3 * SW + 1) * sizeof(double2));
   L.tloc = o;  // special columns, pivot slots, mask; F on special columns; 1/pivots, |pivot|^2
@@ -103,8 +95,6 @@ __host__ __device__ inline Layout cluster_layout(int np, int nq, int box_size, i
   o += al16((size_t)2 * SW * WCH * sizeof(double));
   L.scr = o;
   o += al16(sizeof(Scratch));
-  L.gjl = o;
-  o += al16(sizeof(GjLocal));
   L.g2s = o;
   o += al16((size_t)np * sizeof(double));
   L.rsum = o;
@@ -199,14 +189,12 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
   const Layout LY = cluster_layout(NP, RK4 ? 3 : 2, p.box_size, p.ndiff);
   double* const planes = reinterpret_cast<double*>(smem + LY.planes);
   double2* const boxes = reinterpret_cast<double2*>(smem + LY.boxes);
-  double2* const fpub = reinterpret_cast<double2*>(smem + LY.fpub);  // [2][NP] published multipliers
-  double2* const floc = reinterpret_cast<double2*>(smem + LY.floc);  // [NP] local copy
+  double2* const fpub = reinterpret_cast<double2*>(smem + LY.fpub);  // [2][NP] panel multiplier rows
   double2* const tpub = reinterpret_cast<double2*>(smem + LY.tpub);  // panel table
   double2* const tloc = reinterpret_cast<double2*>(smem + LY.tloc);  // consumer tables
   double* const wchr = reinterpret_cast<double*>(smem + LY.wch);     // [16][WCH]
   double* const wchi = wchr + SW * WCH;
   Scratch* const sc = reinterpret_cast<Scratch*>(smem + LY.scr);
-  GjLocal* const gl = reinterpret_cast<GjLocal*>(smem + LY.gjl);
   double* const g2s = reinterpret_cast<double*>(smem + LY.g2s);
   double* const rsum = reinterpret_cast<double*>(smem + LY.rsum);
   double* const dsum = reinterpret_cast<double*>(smem + LY.dsum);

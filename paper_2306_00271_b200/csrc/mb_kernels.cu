@@ -449,6 +449,11 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
   double* Ai = Xi[0];
   double* Nr = Xr[1];
   double* Ni = Xi[1];
+  // splitting: X2 holds the re+im sum planes of the two Q buffers (GEMM B-side
+  // 3M operand); the RHST borrows them as its saved-Q pair and rebuilds them
+  double* As = Xr[2];
+  double* Ns = Xi[2];
+  constexpr bool XS = !RK4 && NP >= 64;  // measured: a small gain at NP = 64 only
   for (int i = tid; i < p.ndiff; i += C::NT) sboxpos[i] = p.boxpos[i];
   for (int i = tid; i < kMaxOcc; i += C::NT) {
     okick[i] = p.occ_kick[i];
@@ -552,6 +557,8 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
 #pragma unroll
       for (int q = 0; q < 4; ++q) q0[q] += c * P[mb][nb][q];
       own.st(Nr, Ni, mb, nb, q0);
+      if constexpr (XS)
+        *reinterpret_cast<double2*>(Ns + sw<NP>(own.r(mb), own.c(nb))) = make_double2(q0[0] + q0[2], q0[1] + q0[3]);
     }
     double* t = Ar;
     Ar = Nr;
@@ -559,7 +566,17 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
     t = Ai;
     Ai = Ni;
     Ni = t;
+    t = As;
+    As = Ns;
+    Ns = t;
   };
+  // sum plane of the current Q (splitting); after the initial state and RHST
+  auto rebuild_sum = [&]() {
+    if constexpr (XS)
+      for (int w = tid; w < NP * NP; w += C::NT) As[w] = Ar[w] + Ai[w];
+  };
+  rebuild_sum();
+  __syncthreads();
   PROF_MARK(7);
   for (int step = 0; step < L; ++step) {
     if constexpr (RK4) {
@@ -710,7 +727,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
         const int nr = last ? (fsal ? 1 : 0) : r + 1;
         if (p.variant == 0) drift_swap(odrift[r]);  // ABA: drift before kick r
         double2* box = begin_occ(nstep, nr);
-        gemm_box<C>(acc, box, soff, raddr, Ar, Ai, own.col0, lane, kmax);
+        gemm_box<C, XS>(acc, box, soff, raddr, Ar, Ai, own.col0, lane, kmax, As);
         PROF_MARK(1);
         end_occ(nstep, nr);
         const double kc = (fsal && last && step + 1 < L) ? p.fsal_kick : okick[r];
@@ -777,6 +794,8 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
       own.load(Sr, Si, P);
       __syncthreads();
       set_identity<C>(Ar, Ai, n, tid);
+      __syncthreads();
+      rebuild_sum();
       ++rhst;
       __syncthreads();
     }

@@ -121,11 +121,14 @@ __device__ __forceinline__ void cmma(double (&acc)[C::MB][C::NB][4], const doubl
 // one DADD per fragment. Normwise error stays O(eps |U| |X|) (Higham, "Stability
 // of a method for multiplying complex matrices with three real matrix
 // multiplications", 1992), which is the bound the propagation needs.
-template <class C>
+// Xs (XS = true): a plane holding Xr + Xi, kept by the writer of X, so the
+// B-side sums cost a shared load instead of a DADD on the FP64 pipe that the
+// DMMAs occupy.
+template <class C, bool XS = false>
 __device__ __forceinline__ void gemm_box(double (&acc)[C::MB][C::NB][4], const double2* __restrict__ box,
                                          const int* __restrict__ soff, const int (&raddr)[C::MB],
                                          const double* __restrict__ Xr, const double* __restrict__ Xi,
-                                         int col0, int lane, int kmax) {
+                                         int col0, int lane, int kmax, const double* __restrict__ Xs = nullptr) {
   const int kl = lane & 3, cl = lane >> 2;
   if constexpr (C::M3) {
     double t1[C::MB][C::NB][2], t2[C::MB][C::NB][2], t3[C::MB][C::NB][2];
@@ -154,7 +157,10 @@ __device__ __forceinline__ void gemm_box(double (&acc)[C::MB][C::NB][4], const d
         const int o = sw<C::NP>(k, col0 + nb * 8 + cl);
         br[nb] = Xr[o];
         bi[nb] = Xi[o];
-        bs[nb] = br[nb] + bi[nb];
+        if constexpr (XS)
+          bs[nb] = Xs[o];
+        else
+          bs[nb] = br[nb] + bi[nb];
       }
 #pragma unroll
       for (int mb = 0; mb < C::MB; ++mb)
