@@ -238,6 +238,7 @@ def main():
     ck = clocks.stop()
     eta, rho, status = plan.results()
     rhst_mean = float(status["rhst"].mean())
+    rhst_piv = float(status["rhst_pivoting"].mean())
     plan.close()
 
     pot_bytes = float(info["coef_bytes"])  # 16 B x structures x slots x ndiff
@@ -324,7 +325,7 @@ def main():
                                    "note": "K1 is ~0.1% of the step; at cfg1 it is bound by its exp() evaluations"},
             "cpu_baseline": cb, "e2e": e2e, "gpu_launches": launches,
             "kernel_ms": {"potential": pot / args.steps, "propagate": ms_prop},
-            "rhst_per_point": rhst_mean, "wall_s_timed": t_wall, "clocks": ck,
+            "rhst_per_point": rhst_mean, "rhst_pivoting_per_point": rhst_piv, "wall_s_timed": t_wall, "clocks": ck,
         }
         print(json.dumps(line), flush=True)
     if dist:

@@ -161,7 +161,8 @@ typedef struct {
   int code;        /* MB_POINT_* */
   int step;        /* BreakdownError::step */
   int rhst_count;  /* SolveStats::rhst_transforms */
-  int reserved;
+  int rhst_pivoting; /* EXTENSION: transforms whose Q was not strictly row-dominant
+                        (Gershgorin estimate +inf), i.e. needed a pivoting solve */
 } mb_point_status;
 
 /* ---- context ----------------------------------------------------------- */

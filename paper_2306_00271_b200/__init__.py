@@ -120,7 +120,8 @@ class _Pair(C.Structure):
     _fields_ = [("structure", C.c_int), ("theta0_deg", C.c_double), ("theta1_deg", C.c_double)]
 
 
-POINT_STATUS_DTYPE = np.dtype([("code", np.int32), ("step", np.int32), ("rhst", np.int32), ("reserved", np.int32)])
+POINT_STATUS_DTYPE = np.dtype([("code", np.int32), ("step", np.int32), ("rhst", np.int32),
+                               ("rhst_pivoting", np.int32)])
 POINT_OK, POINT_NONFINITE, POINT_RHST, POINT_EXTRACTION = 0, 1, 2, 3
 
 _lib = None

@@ -868,7 +868,7 @@ int collect_results(mb_plan* pl, double* eta, double* rho, mb_point_status* stat
   cuda_check(cudaStreamSynchronize(st), "D2H");
   if (status)
     for (std::size_t i = 0; i < stv.size(); ++i)
-      status[i] = mb_point_status{stv[i].code, stv[i].step, stv[i].rhst, 0};
+      status[i] = mb_point_status{stv[i].code, stv[i].step, stv[i].rhst, stv[i].reserved};
   for (std::size_t i = 0; i < stv.size(); ++i) {
     if (stv[i].code == MB_POINT_OK) continue;
     const std::string where = " (pair " + std::to_string(i) + ", step " + std::to_string(stv[i].step) + ")";

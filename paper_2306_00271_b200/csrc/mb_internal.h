@@ -12,7 +12,7 @@ constexpr int kMaxOcc = 32;  // kick occurrences (or RK stages) per step
 
 // Point status on the device (mirrors mb_point_status)
 struct PointStatus {
-  int code, step, rhst, reserved;
+  int code, step, rhst, reserved;  // reserved: RHSTs that took the pivoting solve
 };
 
 // ---- K1: slice-potential coefficients --------------------------------------

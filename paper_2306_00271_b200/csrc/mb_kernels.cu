@@ -516,7 +516,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
   long cur_slot = slot_of(0, 0);
   issue(cur, cur_slot);
 
-  int rhst = 0;
+  int rhst = 0, npiv = 0;
   int code = 0, fail_step = 0;
   const int nocc = p.nocc;
   const int L = p.nsteps;
@@ -797,6 +797,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
       __syncthreads();
       rebuild_sum();
       ++rhst;
+      if (!isfinite(xi)) ++npiv;
       __syncthreads();
     }
     PROF_MARK(5);
@@ -881,7 +882,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
     st.code = code;
     st.step = fail_step;
     st.rhst = rhst;
-    st.reserved = 0;
+    st.reserved = npiv;
     p.status[pair] = st;
   }
 }

@@ -744,6 +744,7 @@ __global__ void __launch_bounds__(NTH, 1) big_gj_kernel(const __grid_constant__ 
     if (tid == 0) {
       PointStatus st = p.status[pair];
       st.rhst += 1;
+      if (!isfinite(p.xi[pair])) st.reserved += 1;
       p.status[pair] = st;
     }
   } else {

@@ -37,7 +37,7 @@ plan = mb.Plan(rods, configs.product_fields(w), w.gamma, pairs, opts)
 for _ in range(a.reps):
     plan.execute()
 eta, rho, st = plan.results()
-print(w.name, plan.timing(), plan.info(), "rhst/pt", float(st["rhst"].mean()), "pivoting/pt", float(st["reserved"].mean()))
+print(w.name, plan.timing(), plan.info(), "rhst/pt", float(st["rhst"].mean()), "pivoting/pt", float(st["rhst_pivoting"].mean()))
 prof = plan.profile()
 if sum(prof.values()) > 0:
     tot = sum(list(prof.values())[:8])

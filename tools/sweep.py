@@ -53,5 +53,5 @@ for w in cases:
                       "ms_propagate": best["ms_propagate"], "launches": best["launches"],
                       "points_per_s": len(pairs) / (best["ms_total"] * 1e-3),
                       "tflops_propagate": flops / (best["ms_propagate"] * 1e-3) / 1e12,
-                      "rhst_per_point": float(st["rhst"].mean()), "failed": int((st["code"] != 0).sum()),
+                      "rhst_per_point": float(st["rhst"].mean()), "rhst_pivoting_per_point": float(st["rhst_pivoting"].mean()), "failed": int((st["code"] != 0).sum()),
                       "npad": info["npad"], "plan_s": t_plan}), flush=True)
