@@ -218,10 +218,16 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
   double* const Bi_ = planes + 3 * SW * NP;
   // per-pair L2 scratch: M0 (A), M1 (B), row-major NP x NP planes
   const long NN = (long)NP * NP;
-  double* const M0r = p.scratch + pair * 4 * NN;
+  double* const M0r = p.scratch + pair * 6 * NN;
   double* const M0i = M0r + NN;
   double* const M1r = M0r + 2 * NN;
   double* const M1i = M0r + 3 * NN;
+  // M2: the panel rows of A after factorisation (multiplier rows F), written
+  // by each panel's owner and read by every CTA from L2. DSMEM is the wrong
+  // channel for this broadcast: the owner's shared-memory port would serve
+  // all CS-1 readers (~20 B/clk per SM, producer pays).
+  double* const M2r = M0r + 4 * NN;
+  double* const M2i = M0r + 5 * NN;
 
   const double2* coef = p.coef + (long)p.pair_struct[pair] * p.nslots * p.ndiff;
   const int kmax = (n + 3) & ~3;
@@ -417,6 +423,15 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
       }
       __syncthreads();
     }
+    // publish the panel rows (F) to L2 for the consumers
+    for (int w = tid; w < nk * (NP / 2); w += CNT) {
+      const int lr = w / (NP / 2), j = 2 * (w % (NP / 2));
+      const int so = sw<NP>(lr, j);
+      const long o = (long)(col0 + lr) * NP + j;
+      *reinterpret_cast<double2*>(M2r + o) = *reinterpret_cast<const double2*>(Ar_ + so);
+      *reinterpret_cast<double2*>(M2i + o) = *reinterpret_cast<const double2*>(Ai_ + so);
+    }
+    __syncthreads();
     if (tid == 0) {
       __threadfence();  // tables and rows visible cluster-wide before the flag
       *reinterpret_cast<volatile int*>(tpub + 3 * SW) = sid;
@@ -441,37 +456,32 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
     CPROF(11);
     if (crank == 0) factor_panel(sid);
     CPROF(8);
-    const int row = tid >> 3, cg8 = tid & 7;  // 32 local rows (16 A, 16 B) x 8 threads
-    const bool isA = row < SW;
-    const int lr = isA ? row : row - SW;
-    const int gi = col0 + lr;
-    double* Xr = isA ? Ar_ : Br_;
-    double* Xi = isA ? Ai_ : Bi_;
-    int* scol = reinterpret_cast<int*>(tloc);            // [32] special columns
-    int* pslot = scol + 2 * SW;                          // [16] slot of p_k
+    int* scol = reinterpret_cast<int*>(tloc);                   // [32] special columns
+    int* pslot = scol + 2 * SW;                                 // [16] slot of p_k
     unsigned* smask = reinterpret_cast<unsigned*>(pslot + SW);  // [NP/32] special-column bitmask
-    int* sn = reinterpret_cast<int*>(smask + NP / 32);   // [1] special count
-    double2* fs = tloc + 8 * SW;                         // [16][32] F on special columns
-    double2* linv = fs + 2 * SW * SW;                    // [16] 1/pivot
+    int* sn = reinterpret_cast<int*>(smask + NP / 32);          // [1] special count
+    int* lpp = sn + 1;                                          // [16] pivot columns
+    double2* fs = tloc + 8 * SW;                                // [16][32] F on special columns
+    double2* linv = fs + 2 * SW * SW;                           // [16] 1/pivot
+    double* lpv = reinterpret_cast<double*>(linv + SW);         // [16] |pivot|^2
+    // 16 threads per row: lr = tid / 16 (16 rows), slots cg and cg + 16
+    const int lr = tid >> 4, cg = tid & 15, gi = col0 + lr;
+    const int rbase = lane & ~15;
     bool okb = true;
     for (int b = 0; b < npan; ++b) {
       wait_panel(b, sid);
       CPROF(9);
       const int p0 = b * SW, nk = min(SW, n - p0);
       const double2* rt = cl.map_shared_rank(tpub, b);
-      const int* rpp = reinterpret_cast<const int*>(rt + 2 * SW);
-      const double* rpv = reinterpret_cast<const double*>(rt + SW);
-      const double* war = cl.map_shared_rank(Ar_, b);
-      const double* wai = cl.map_shared_rank(Ai_, b);
-      // special columns: the panel's, then pivots outside it (first occurrence)
-      int* lpp = pslot + SW + NP / 32 + 1;  // [16] local copy of the pivot columns
-      double* lpv = reinterpret_cast<double*>(linv + SW);  // [16]
+      const double* war = M2r + (long)p0 * NP;  // panel rows, row-major, ld NP
+      const double* wai = M2i + (long)p0 * NP;
       if (tid < SW) {
         linv[tid] = rt[tid];
-        lpp[tid] = rpp[tid];
-        lpv[tid] = rpv[tid];
+        lpp[tid] = reinterpret_cast<const int*>(rt + 2 * SW)[tid];
+        lpv[tid] = reinterpret_cast<const double*>(rt + SW)[tid];
       }
       __syncthreads();
+      // special columns: the panel's, then pivots outside it (first occurrence)
       if (tid == 0) {
         int cnt = SW;
         bool fail = false;
@@ -509,101 +519,111 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
         if (lk < nk && j >= 0 && j < n) {
           const int k = p0 + lk, pk = lpp[lk];
           const int jj = (j == pk) ? k : j;  // F_k[p_k] = A[k][k]
-          if (j != k) f = make_double2(war[sw<NP>(lk, jj)], wai[sw<NP>(lk, jj)]);
+          if (j != k) f = make_double2(__ldcg(war + (long)lk * NP + jj), __ldcg(wai + (long)lk * NP + jj));
         }
         fs[w] = f;
       }
       __syncthreads();
-      const bool act = gi < n && (isA ? gi >= p0 + SW : true);
-      // (A) sequential ops on the special columns: thread cg8 holds slots cg8 + 8u
-      double2 val[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int j = scol[cg8 + 8 * u];
-        val[u] = (act && j >= 0) ? make_double2(Xr[sw<NP>(lr, j)], Xi[sw<NP>(lr, j)]) : make_double2(0.0, 0.0);
-      }
-      double2 xk[SW];
-      const int rbase = lane & ~7;
-#pragma unroll
-      for (int lk = 0; lk < SW; ++lk) {
-        xk[lk] = make_double2(0.0, 0.0);
-        if (lk < nk) {
-          const int ps = pslot[lk], ks = lk;
-          const double2 inv = linv[lk];
-          auto pick = [&](int sl) {
-            const int u = sl >> 3;
-            double2 v = val[0];
-            if (u == 1) v = val[1];
-            if (u == 2) v = val[2];
-            if (u == 3) v = val[3];
-            return make_double2(__shfl_sync(0xffffffffu, v.x, rbase | (sl & 7)),
-                                __shfl_sync(0xffffffffu, v.y, rbase | (sl & 7)));
-          };
-          const double2 xp = pick(ps);
-          const double2 xold = pick(ks);
-          const double2 x = cmul(xp, inv);
-          xk[lk] = x;
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int sl = cg8 + 8 * u;
-            const double2 f = fs[lk * 2 * SW + sl];
-            const double2 v = (sl == ps) ? xold : val[u];
-            double2 nv = make_double2(v.x - (f.x * x.x - f.y * x.y), v.y - (f.x * x.y + f.y * x.x));
-            val[u] = (sl == ks) ? x : nv;
-          }
-        }
-      }
-      if (act) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int j = scol[cg8 + 8 * u];
-          if (j >= 0) {
-            Xr[sw<NP>(lr, j)] = val[u].x;
-            Xi[sw<NP>(lr, j)] = val[u].y;
-          }
-        }
-      }
       CPROF(10);
-      // (B) other columns: X[i][j] -= sum_k x_k F_k[j] (F_k[j] = A[k][j] there)
-      for (int j0 = 0; j0 < n; j0 += WCH) {
-        __syncthreads();  // previous chunk consumed (and the special write-back done)
-        for (int w = tid; w < SW * (WCH / 2); w += CNT) {
-          const int t = w / (WCH / 2), jj = 2 * (w % (WCH / 2));
-          const int j = j0 + jj;
-          double2 a = make_double2(0.0, 0.0), c = a;
-          if (t < nk && j < NP) {
-            const int o = sw<NP>(t, j);
-            a = *reinterpret_cast<const double2*>(war + o);
-            c = *reinterpret_cast<const double2*>(wai + o);
+      // apply the panel's 16 ops to the own A rows (half 0) or B rows (half 1)
+      auto consume = [&](int half) {
+        const bool isA = half == 0;
+        if (isA && col0 + SW <= p0 + SW) return;  // CTA-uniform: no A rows below the panel
+        double* Xr = isA ? Ar_ : Br_;
+        double* Xi = isA ? Ai_ : Bi_;
+        const bool act = gi < n && (isA ? gi >= p0 + SW : true);
+        // (A) sequential ops on the special columns
+        double2 val[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int j = scol[cg + 16 * u];
+          val[u] = (act && j >= 0) ? make_double2(Xr[sw<NP>(lr, j)], Xi[sw<NP>(lr, j)]) : make_double2(0.0, 0.0);
+        }
+        double2 xk[SW];
+#pragma unroll
+        for (int lk = 0; lk < SW; ++lk) {
+          xk[lk] = make_double2(0.0, 0.0);
+          if (lk < nk) {
+            const int ps = pslot[lk], ks = lk;
+            auto pick = [&](int sl) {
+              const double2 v = (sl >> 4) ? val[1] : val[0];
+              return make_double2(__shfl_sync(0xffffffffu, v.x, rbase | (sl & 15)),
+                                  __shfl_sync(0xffffffffu, v.y, rbase | (sl & 15)));
+            };
+            const double2 xp = pick(ps);
+            const double2 xold = pick(ks);
+            const double2 x = cmul(xp, linv[lk]);
+            xk[lk] = x;
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const int sl = cg + 16 * u;
+              const double2 f = fs[lk * 2 * SW + sl];
+              const double2 v = (sl == ps) ? xold : val[u];
+              const double2 nv = make_double2(v.x - (f.x * x.x - f.y * x.y), v.y - (f.x * x.y + f.y * x.x));
+              val[u] = (sl == ks) ? x : nv;
+            }
+          }
+        }
+        if (act) {
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int j = scol[cg + 16 * u];
+            if (j >= 0) {
+              Xr[sw<NP>(lr, j)] = val[u].x;
+              Xi[sw<NP>(lr, j)] = val[u].y;
+            }
+          }
+        }
+        // (B) other columns: X[i][j] -= sum_k x_k F_k[j] (F_k[j] = A[k][j]),
+        // F chunks from the owner through DSMEM, next chunk prefetched into
+        // registers while the current one is applied
+        const int ldt = tid / (WCH / 2), ldj = 2 * (tid % (WCH / 2));  // 16 x 32 chunk, one double2 each
+        auto fetch = [&](int j0, double2& a, double2& c) {
+          const int j = j0 + ldj;
+          a = make_double2(0.0, 0.0);
+          c = a;
+          if (ldt < nk && j < NP) {
+            const long o = (long)ldt * NP + j;
+            a = __ldcg(reinterpret_cast<const double2*>(war + o));
+            c = __ldcg(reinterpret_cast<const double2*>(wai + o));
           }
           if (j >= n || ((smask[j >> 5] >> (j & 31)) & 1u)) a.x = c.x = 0.0;
           if (j + 1 >= n || ((smask[(j + 1) >> 5] >> ((j + 1) & 31)) & 1u)) a.y = c.y = 0.0;
-          *reinterpret_cast<double2*>(wchr + t * WCH + jj) = a;
-          *reinterpret_cast<double2*>(wchi + t * WCH + jj) = c;
-        }
-        __syncthreads();
-        if (act) {
+        };
+        double2 na, nc;
+        fetch(0, na, nc);
+        for (int j0 = 0; j0 < n; j0 += WCH) {
+          __syncthreads();  // previous chunk consumed (and the special write-back done)
+          *reinterpret_cast<double2*>(wchr + ldt * WCH + ldj) = na;
+          *reinterpret_cast<double2*>(wchi + ldt * WCH + ldj) = nc;
+          __syncthreads();
+          if (j0 + WCH < n) fetch(j0 + WCH, na, nc);
+          if (act) {
 #pragma unroll
-          for (int u = 0; u < WCH / 8; ++u) {
-            const int jj = cg8 + 8 * u, j = j0 + jj;
-            if (j >= n) continue;
-            const int o = sw<NP>(lr, j);
-            double xr = Xr[o], xi = Xi[o];
+            for (int u = 0; u < WCH / 16; ++u) {
+              const int jj = cg + 16 * u, j = j0 + jj;
+              if (j >= n) continue;
+              const int o = sw<NP>(lr, j);
+              double xr = Xr[o], xi = Xi[o];
 #pragma unroll
-            for (int t = 0; t < SW; ++t) {
-              const double wr = wchr[t * WCH + jj], wi = wchi[t * WCH + jj];
-              xr -= xk[t].x * wr - xk[t].y * wi;
-              xi -= xk[t].x * wi + xk[t].y * wr;
+              for (int t = 0; t < SW; ++t) {
+                const double wr = wchr[t * WCH + jj], wi = wchi[t * WCH + jj];
+                xr -= xk[t].x * wr - xk[t].y * wi;
+                xi -= xk[t].x * wi + xk[t].y * wr;
+              }
+              Xr[o] = xr;
+              Xi[o] = xi;
             }
-            Xr[o] = xr;
-            Xi[o] = xi;
           }
         }
-      }
-      __syncthreads();
+        __syncthreads();
+      };
+      consume(0);  // A rows first: the next owner's panel depends on them
       CPROF(11);
-      if (crank == b + 1) factor_panel(sid);  // own A rows are final for panel b+1
+      if (crank == b + 1) factor_panel(sid);
       CPROF(8);
+      consume(1);
+      CPROF(11);
     }
     // an owner's rows and table are immutable for the rest of the solve, so
     // consumers may lag; one barrier before any of them is reused

@@ -729,7 +729,7 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
     pl->big = big;
     pl->cluster = cluster;
     pl->stride = (int)stride;
-    if (cluster) p.scratch = dev_alloc<double>(pl, (std::size_t)npairs * 4 * npad * npad);
+    if (cluster) p.scratch = dev_alloc<double>(pl, (std::size_t)npairs * 6 * npad * npad);
     if (big) {
       mbx::BigParams& b = pl->bp;
       b.n = n;

@@ -70,7 +70,7 @@ struct PropagateParams {
   double2* rho;               // [npairs][n]
   PointStatus* status;        // [npairs]
   unsigned long long* prof;   // [8] phase cycles (MB_PROFILE builds), may be null
-  double* scratch;            // cluster kernel: per pair 4 NP^2 doubles (RHST / surface solve)
+  double* scratch;            // cluster kernel: per pair 6 NP^2 doubles (RHST / surface solve)
 };
 
 // ---- large-N batched path (mb_large.cu): state in HBM, one launch per kick
