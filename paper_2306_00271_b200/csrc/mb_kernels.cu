@@ -916,10 +916,33 @@ static cudaError_t launch_cfg(const PropagateParams& p, cudaStream_t st) {
 // CTA bound; rk4 at NP <= 32 (P, SQ, acc) fits 128 registers with narrower
 // tiles and gains resident CTAs per SM; rk4 at NP = 64 runs the splitting
 // tile (C64) with the K-sum folded into the Q plane (16 warps spill)
-using C16 = Cfg<16, 1, 2, 1, true>;
-using C32 = Cfg<32, 2, 2, 1, true>;
-using C16R = Cfg<16, 2, 2, 4, true>;  // 4 warps, 8x8 tiles, 4 CTAs/SM
-using C32R = Cfg<32, 4, 2, 2, true>;  // 8 warps, 8x16 tiles, 2 CTAs/SM
+// tile variants (WM, WN, CTAs/SM) selectable at build time for tuning sweeps
+// (round-1 sweep on B200, tools/sweep.py cfg2 + cfg4 N=15/31: 4 warps x 3
+// CTAs/SM at NP=32 beat 8 warps x 2 by 12% for rk4 and 3% for sp6)
+#ifndef MB_C32_WM
+#define MB_C32_WM 2
+#define MB_C32_WN 2
+#define MB_C32_MINB 3
+#endif
+#ifndef MB_C32R_WM
+#define MB_C32R_WM 2
+#define MB_C32R_WN 2
+#define MB_C32R_MINB 3
+#endif
+#ifndef MB_C16_WM
+#define MB_C16_WM 1
+#define MB_C16_WN 2
+#define MB_C16_MINB 4
+#endif
+#ifndef MB_C16R_WM
+#define MB_C16R_WM 2
+#define MB_C16R_WN 2
+#define MB_C16R_MINB 4
+#endif
+using C16 = Cfg<16, MB_C16_WM, MB_C16_WN, MB_C16_MINB, true>;
+using C32 = Cfg<32, MB_C32_WM, MB_C32_WN, MB_C32_MINB, true>;
+using C16R = Cfg<16, MB_C16R_WM, MB_C16R_WN, MB_C16R_MINB, true>;  // 4 warps, 8x8 tiles, 4 CTAs/SM
+using C32R = Cfg<32, MB_C32R_WM, MB_C32R_WN, MB_C32R_MINB, true>;  // 4 warps, 16x16 tiles, 3 CTAs/SM
 using C64 = Cfg<64, 4, 2, 1, true>;
 
 int propagate_supported(int n, int rk4) {
