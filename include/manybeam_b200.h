@@ -42,6 +42,8 @@ extern "C" {
 #define MB_POINT_NONFINITE 1   /* "propagation state went nonfinite" */
 #define MB_POINT_RHST 2        /* "stabilizing transform: ..." (zero pivot or residual > 1e-10) */
 #define MB_POINT_EXTRACTION 3  /* "reflection extraction: ..." (zero pivot) */
+#define MB_POINT_BULK_READ 4   /* "bulk reflection read: ..." (BreakdownError, step = period) */
+#define MB_POINT_BULK_CONVERGENCE 5 /* ConvergenceError: bulk R did not settle (proposed.cpp:338-341) */
 
 typedef struct mb_context mb_context;
 typedef struct mb_plan mb_plan;
@@ -84,7 +86,8 @@ int mb_rods_build(const mb_lattice* lattice, double cutoff, int first_n, int* n,
 typedef struct {
   int kind;
   double z_bottom; /* A, < 0 */
-  int has_bulk_period; /* bulk seeding is the §8f "next" row: rejected for now */
+  int has_bulk_period; /* bulk seed R_init per pair (compute_bulk_reflection_proposed,
+                          proposed.cpp:311-342); resident kernel (N <= 64) only */
   double bulk_period;
   /* MB_FIELD_GAUSSIAN_LAYERS: layers[nlayers][5] = z_center, amplitude,
    * sigma_xy, sigma_z, absorption */

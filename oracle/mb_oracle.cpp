@@ -396,8 +396,9 @@ PotentialField PotentialField::tabulated(double zb, std::vector<double> grid,
   return f;
 }
 
-PotentialField PotentialField::atoms(double zb, AtomModel model) {  // EXTENSION
+PotentialField PotentialField::atoms(double zb, AtomModel model, std::optional<double> period) {  // EXTENSION
   validate_bottom(zb);
+  validate_period(zb, period);
   if (!(model.cell_area > 0.0)) throw ConfigError("atoms: cell area must be positive");
   for (const AtomSite& a : model.atoms) {
     if (a.species < 0 || a.species >= (int)model.species.size())
@@ -412,6 +413,7 @@ PotentialField PotentialField::atoms(double zb, AtomModel model) {  // EXTENSION
   PotentialField f;
   f.kind = Kind::Atoms;
   f.z_bottom = zb;
+  f.bulk_period = period;
   f.model = std::move(model);
   return f;
 }

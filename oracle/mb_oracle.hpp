@@ -169,7 +169,7 @@ class PotentialField {
   static PotentialField tabulated(double z_bottom, std::vector<double> z_grid,
                                   std::vector<TabulatedEntry> entries,
                                   std::optional<double> bulk_period = {});
-  static PotentialField atoms(double z_bottom, AtomModel model);
+  static PotentialField atoms(double z_bottom, AtomModel model, std::optional<double> bulk_period = {});
   Kind kind = Kind::Zero;
   double z_bottom = -1;
   std::optional<double> bulk_period;

@@ -184,7 +184,7 @@ PYBIND11_MODULE(mb_oracle, m) {
           [](double zb, py::array_t<double, py::array::forcecast> xyz, py::array_t<int, py::array::forcecast> species,
              py::array_t<double, py::array::forcecast> B, py::array_t<double, py::array::forcecast> ff_a,
              py::array_t<double, py::array::forcecast> ff_b, double cell_area, double gamma_L, double particle_sign,
-             double absorption) {
+             double absorption, py::object period) {
             AtomModel M;
             auto x = xyz.unchecked<2>();
             auto s = species.unchecked<1>();
@@ -205,10 +205,11 @@ PYBIND11_MODULE(mb_oracle, m) {
             M.gamma_L = gamma_L;
             M.particle_sign = particle_sign;
             M.absorption = absorption;
-            return PotentialField::atoms(zb, std::move(M));
+            return PotentialField::atoms(zb, std::move(M), opt_period(period));
           },
           py::arg("z_bottom"), py::arg("xyz"), py::arg("species"), py::arg("B"), py::arg("ff_a"), py::arg("ff_b"),
-          py::arg("cell_area"), py::arg("gamma_L"), py::arg("particle_sign"), py::arg("absorption"))
+          py::arg("cell_area"), py::arg("gamma_L"), py::arg("particle_sign"), py::arg("absorption"),
+          py::arg("bulk_period") = py::none())
       .def_readonly("z_bottom", &PotentialField::z_bottom);
   py::class_<BoundPotential>(m, "BoundPotential")
       .def(py::init<const PotentialField&, const RodSet&>(), py::keep_alive<1, 2>())

@@ -314,7 +314,8 @@ class PotentialField:
                               bulk_period=bulk_period)
 
     @staticmethod
-    def atoms(z_bottom, xyz, species, B, ff_a, ff_b, cell_area, gamma_L, particle_sign, absorption=0.1):
+    def atoms(z_bottom, xyz, species, B, ff_a, ff_b, cell_area, gamma_L, particle_sign, absorption=0.1,
+              bulk_period=None):
         """EXTENSION: atom list (Cartesian A), species index, Debye-Waller B (A^2),
         4-Gaussian form factors ff_a (A) / ff_b (A^2) per species."""
         return PotentialField(MB_FIELD_ATOMS, z_bottom,
@@ -324,7 +325,8 @@ class PotentialField:
                               ff_a=np.ascontiguousarray(ff_a, np.float64).reshape(-1, 4),
                               ff_b=np.ascontiguousarray(ff_b, np.float64).reshape(-1, 4),
                               cell_area=float(cell_area), gamma_L=float(gamma_L),
-                              particle_sign=float(particle_sign), absorption=float(absorption))
+                              particle_sign=float(particle_sign), absorption=float(absorption),
+                              bulk_period=bulk_period)
 
     def _c(self):
         f = _Field()

@@ -62,6 +62,7 @@ class Workload:
     pairs: np.ndarray = None  # [npairs][3]: structure, theta0, theta1 (default: all x all)
     theta1: List[float] = field(default_factory=lambda: [0.0])
     absorption: float = 0.1
+    bulk_period: float = None  # bulk seed below z_bottom (compute_bulk_reflection_proposed); None: R_init = 0
 
     @property
     def cell_area(self):
@@ -101,7 +102,7 @@ class Workload:
                      z_bottom if z_bottom is not None else self.z_bottom,
                      slices or self.slices, self.method, list(theta0 if theta0 is not None else self.theta0),
                      [self.structures[i] for i in (structures if structures is not None else range(len(self.structures)))],
-                     None, list(self.theta1), self.absorption)
+                     None, list(self.theta1), self.absorption, self.bulk_period)
         return w
 
 
@@ -223,4 +224,4 @@ def product_fields(w):
     from . import PotentialField
     ff_a, ff_b = form_factors()
     return [PotentialField.atoms(w.z_bottom, s.xyz, s.species, s.B, ff_a, ff_b, w.cell_area, w.gamma_L, w.sign,
-                                 w.absorption) for s in w.structures]
+                                 w.absorption, bulk_period=w.bulk_period) for s in w.structures]

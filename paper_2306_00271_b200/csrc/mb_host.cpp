@@ -9,6 +9,8 @@
 #include <algorithm>
 #include <cmath>
 #include <complex>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <map>
@@ -277,8 +279,11 @@ Schedule make_schedule(const mb_stepper& s) {
 void validate_field(const mb_field& f) {
   if (!(f.z_bottom < 0.0) || !std::isfinite(f.z_bottom))
     fail(MB_ERR_CONFIG, "potential: z_bottom must be negative and finite");
-  if (f.has_bulk_period)
-    fail(MB_ERR_CONFIG, "potential: bulk-period seeding (compute_bulk_reflection_proposed) is not supported on the device path yet");
+  if (f.has_bulk_period) {  // potential.cpp:22-28
+    if (!(f.bulk_period > 0.0) || !std::isfinite(f.bulk_period))
+      fail(MB_ERR_CONFIG, "potential: bulk_period must be positive and finite");
+    if (f.bulk_period > -f.z_bottom + 1e-9) fail(MB_ERR_CONFIG, "potential: bulk_period must not exceed |z_bottom|");
+  }
   switch (f.kind) {
     case MB_FIELD_ZERO:
       return;
@@ -364,12 +369,17 @@ Tabulated bind_tabulated(const mb_field& f, const RodTables& rt) {
   }
   return t;
 }
-double map_z(double z, double zb) {  // potential.cpp:152-167 without bulk
+double map_z(double z, double zb, double period = 0.0) {  // potential.cpp:152-167
   if (z > 1e-9 || !std::isfinite(z)) fail(MB_ERR_DOMAIN, "potential evaluated above the surface");
   if (z > 0.0) z = 0.0;
   if (z >= zb) return z;
   if (z >= zb - 1e-9) return zb;
-  fail(MB_ERR_DOMAIN, "potential evaluated below z_bottom without a bulk period");
+  if (!(period > 0.0)) fail(MB_ERR_DOMAIN, "potential evaluated below z_bottom without a bulk period");
+  const double k = std::ceil((zb - z) / period - 1e-12);
+  double zm = z + k * period;
+  if (zm < zb) zm += period;
+  if (zm > zb + period) zm = zb + period;
+  return std::min(zm, 0.0);
 }
 void eval_tabulated(const Tabulated& t, double zb, double z, cd* out) {
   const double zm = map_z(z, zb);
@@ -482,6 +492,9 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
   for (int f = 0; f < nfields; ++f) {
     validate_field(fields[f]);
     if (fields[f].z_bottom != zb) fail(MB_ERR_CONFIG, "batch: every field must share z_bottom");
+    if ((fields[f].has_bulk_period != 0) != (fields[0].has_bulk_period != 0) ||
+        (fields[f].has_bulk_period && fields[f].bulk_period != fields[0].bulk_period))
+      fail(MB_ERR_CONFIG, "batch: every field must share the bulk period");
     if (fields[f].kind != fields[0].kind) fail(MB_ERR_CONFIG, "batch: every field must be of one kind");
   }
   // resident kernel (state on chip) when it fits; 64 < n <= 256: one cluster
@@ -491,6 +504,8 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
   int npad = mbx::propagate_supported(n, stepper->algorithm == MB_STEP_RK4);
   if (opts->path == 1 && !npad) fail(MB_ERR_CONFIG, "resident kernel does not cover this rod count / stepper");
   if (opts->path == 2 || opts->path == 3) npad = 0;
+  if (fields[0].has_bulk_period && !npad)
+    fail(MB_ERR_CONFIG, "bulk seeding runs in the resident kernel only (N <= 64, path 0 or 1)");
   bool big = npad == 0;
   if (big) npad = (n + 7) & ~7;
 
@@ -506,16 +521,39 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
   const Schedule sc = make_schedule(*stepper);
   const int K = (int)sc.frac.size();
   const long stride = sc.endpoint_pair() ? K - 1 : K;
-  const long nslots = sc.endpoint_pair() ? L * (K - 1) + 1 : L * K;
-  auto wz = [&](long i) { return (zb * (double)(L - i) + 0.0 * (double)i) / (double)L; };  // StepWindow::z
-  std::vector<double> zslot((std::size_t)nslots);
-  for (long i = 0; i < L; ++i)
-    for (int m = 0; m < K; ++m) {
-      const long slot = i * stride + m;
-      if (slot >= nslots) continue;
-      const double f = sc.frac[m];
-      zslot[(std::size_t)slot] = f == 0.0 ? wz(i) : (f == 1.0 ? wz(i + 1) : wz(i) + f * h);
-    }
+  const long nslots_main = sc.endpoint_pair() ? L * (K - 1) + 1 : L * K;
+  // node heights of a window [z0, z1] in `count` steps (StepWindow::z, node_z)
+  std::vector<double> zslot;
+  auto add_window = [&](double z0, double z1, long count, double hw, double period) {
+    const long ns = sc.endpoint_pair() ? count * (K - 1) + 1 : count * K;
+    const std::size_t base = zslot.size();
+    zslot.resize(base + (std::size_t)ns);
+    auto wz = [&](long i) { return (z0 * (double)(count - i) + z1 * (double)i) / (double)count; };
+    for (long i = 0; i < count; ++i)
+      for (int m = 0; m < K; ++m) {
+        const long slot = i * stride + m;
+        if (slot >= ns) continue;
+        const double f = sc.frac[m];
+        const double z = f == 0.0 ? wz(i) : (f == 1.0 ? wz(i + 1) : wz(i) + f * hw);
+        zslot[base + (std::size_t)slot] = period > 0.0 ? map_z(z, z1, period) : z;
+      }
+  };
+  add_window(zb, 0.0, L, h, 0.0);
+  // bulk window (proposed.cpp:311-321): one period below z_bottom, in
+  // max(1, round(period / dz)) steps of StepWindow::over(zb - p, zb, .); the
+  // potential there is the periodic continuation (map_z)
+  const bool bulk = fields[0].has_bulk_period != 0;
+  long Lb = 0;
+  double hb = 0.0;
+  if (bulk) {
+    if (!(opts->dz > 0.0) || !std::isfinite(opts->dz)) fail(MB_ERR_CONFIG, "sweep: dz must be positive and finite");
+    const double per = fields[0].bulk_period;
+    Lb = std::max(1L, std::lround(per / opts->dz));
+    const double z0b = zb - per;
+    hb = (zb - z0b) / (double)Lb;
+    add_window(z0b, zb, Lb, hb, per);
+  }
+  const long nslots = (long)zslot.size();
 
   // pairs: AngleGrid semantics per pair, BeamGeometry + GammaMatrix::build
   // (geometry.cpp:19-57)
@@ -722,6 +760,22 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
     }
     p.threshold = opts->rhst_threshold;
     p.residual_check = opts->residual_check ? 1 : 0;
+    p.bulk_steps = 0;
+    if (bulk) {  // the same stepper on the bulk window's step hb (BulkOptions defaults)
+      p.bulk_steps = (int)Lb;
+      p.bulk_base = nslots_main;
+      p.bulk_h = hb;
+      for (int r = 0; r < mbx::kMaxOcc; ++r) p.bulk_kick[r] = p.bulk_drift[r] = 0.0;
+      if (!p.rk4) {
+        for (int r = 0; r < stepper->nkick; ++r) p.bulk_kick[r] = hb * stepper->kick[r];
+        for (int r = 0; r < stepper->ndrift; ++r) p.bulk_drift[r] = hb * stepper->drift[r];
+        p.bulk_final_drift = stepper->variant == MB_SPLIT_ABA ? hb * stepper->drift[stepper->ndrift - 1] : 0.0;
+        p.bulk_fsal_kick = hb * (stepper->kick[stepper->nkick - 1] + stepper->kick[0]);
+      }
+      p.bulk_max_periods = 10000;
+      p.bulk_tol = 1e-12;
+      p.bulk_scratch = dev_alloc<double>(pl, (std::size_t)npairs * 2 * npad * npad);
+    }
     p.eta = dev_alloc<double>(pl, (std::size_t)npairs * n);
     p.rho = dev_alloc<double2>(pl, (std::size_t)npairs * n);
     p.status = dev_alloc<mbx::PointStatus>(pl, (std::size_t)npairs);
@@ -875,6 +929,11 @@ int collect_results(mb_plan* pl, double* eta, double* rho, mb_point_status* stat
     if (stv[i].code == MB_POINT_NONFINITE) fail(MB_ERR_BREAKDOWN, "propagation state went nonfinite" + where);
     if (stv[i].code == MB_POINT_RHST)
       fail(MB_ERR_BREAKDOWN, "stabilizing transform: solve_right: singular or ill-conditioned system" + where);
+    if (stv[i].code == MB_POINT_BULK_READ)
+      fail(MB_ERR_BREAKDOWN, "bulk reflection read: solve_right: singular or ill-conditioned system (pair " +
+                                 std::to_string(i) + ", period " + std::to_string(stv[i].step) + ")");
+    if (stv[i].code == MB_POINT_BULK_CONVERGENCE)
+      fail(MB_ERR_CONVERGENCE, "bulk reflection did not settle within 10000 periods (pair " + std::to_string(i) + ")");
     fail(MB_ERR_BREAKDOWN, "reflection extraction: solve_right: singular or ill-conditioned system" + where);
   }
   return MB_OK;

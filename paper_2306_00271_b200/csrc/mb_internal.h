@@ -71,6 +71,14 @@ struct PropagateParams {
   PointStatus* status;        // [npairs]
   unsigned long long* prof;   // [8] phase cycles (MB_PROFILE builds), may be null
   double* scratch;            // cluster kernel: per pair 6 NP^2 doubles (RHST / surface solve)
+  // bulk seeding (proposed.cpp:311-342), resident kernel only; bulk_steps = 0: none
+  int bulk_steps;             // steps per bulk period
+  long bulk_base;             // first table slot of the bulk window
+  double bulk_h, bulk_final_drift, bulk_fsal_kick;
+  double bulk_kick[kMaxOcc], bulk_drift[kMaxOcc];
+  long bulk_max_periods;
+  double bulk_tol;
+  double* bulk_scratch;       // per pair 2 NP^2 doubles: the previous period's R
 };
 
 // ---- large-N batched path (mb_large.cu): state in HBM, one launch per kick

@@ -396,7 +396,7 @@ __device__ bool residual_ok(const double* Or, const double* Oi, const double* Xr
   return (resid <= 1e-10) && !B;
 }
 
-template <class C, bool RK4>
+template <class C, bool RK4, bool BULK>
 __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_constant__ PropagateParams p) {
   constexpr int NP = C::NP, MB = C::MB, NB = C::NB;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -422,7 +422,9 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
   // runtime-indexed stepper tables in shared memory (not the param space)
   double* okick = reinterpret_cast<double*>(ps + 1);  // [kMaxOcc]
   double* odrift = okick + kMaxOcc;                   // [kMaxOcc]
-  int* onode = reinterpret_cast<int*>(odrift + kMaxOcc);
+  double* bkick = odrift + kMaxOcc;                   // [kMaxOcc] bulk window (h_bulk)
+  double* bdrift = bkick + kMaxOcc;                   // [kMaxOcc]
+  int* onode = reinterpret_cast<int*>(bdrift + kMaxOcc);
   int* sboxpos = onode + kMaxOcc;  // [ndiff]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -458,6 +460,8 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
   for (int i = tid; i < kMaxOcc; i += C::NT) {
     okick[i] = p.occ_kick[i];
     odrift[i] = p.occ_drift[i];
+    bkick[i] = p.bulk_kick[i];
+    bdrift[i] = p.bulk_drift[i];
     onode[i] = p.occ_node[i];
   }
   // box holes (positions no rod difference maps to) are read for the padded
@@ -503,8 +507,20 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
   constexpr bool SQR = RK4 && NP <= 32;
   double SQ[SQR ? MB : 1][SQR ? NB : 1][4];
 
-  // table pipeline: slot of occurrence (step, r) = step*stride + node
-  auto slot_of = [&](int step, int r) -> long { return (long)step * p.slot_stride + onode[r]; };
+  // the propagation window: the slab (main) or one bulk period (bulk seeding,
+  // proposed.cpp:311-342); its node slots start at wbase in the table
+  // (BULK = false: every window parameter is the slab's, read from the
+  // parameter space; the bulk machinery compiles away)
+  bool bulk_phase = BULK && p.bulk_steps > 0;
+  auto WL = [&]() -> int { return (BULK && bulk_phase) ? p.bulk_steps : p.nsteps; };
+  auto wbase = [&]() -> long { return (BULK && bulk_phase) ? p.bulk_base : 0L; };
+  auto wh = [&]() -> double { return (BULK && bulk_phase) ? p.bulk_h : p.h; };
+  auto wfin = [&]() -> double { return (BULK && bulk_phase) ? p.bulk_final_drift : p.final_drift; };
+  auto wfsal = [&]() -> double { return (BULK && bulk_phase) ? p.bulk_fsal_kick : p.fsal_kick; };
+  auto wkick = [&](int r) -> double { return (BULK && bulk_phase) ? bkick[r] : okick[r]; };
+  auto wdrift = [&](int r) -> double { return (BULK && bulk_phase) ? bdrift[r] : odrift[r]; };
+  // table pipeline: slot of occurrence (step, r) = base + step*stride + node
+  auto slot_of = [&](int step, int r) -> long { return wbase() + (long)step * p.slot_stride + onode[r]; };
   auto issue = [&](double2* dst, long slot) {
     const double2* src = coef + slot * p.ndiff;
     for (int d = gtid; d < p.ndiff; d += GNT) cp_async16(dst + sboxpos[d], src + d);
@@ -513,13 +529,11 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
   double2* cur = boxes + (2 * wn) * p.box_size;
   double2* nxt = cur + p.box_size;
   __syncthreads();  // sboxpos ready
-  long cur_slot = slot_of(0, 0);
-  issue(cur, cur_slot);
+  long cur_slot = -1;
 
   int rhst = 0, npiv = 0;
   int code = 0, fail_step = 0;
   const int nocc = p.nocc;
-  const int L = p.nsteps;
   const bool fsal = !RK4 && p.fsal && p.variant == 1;
 
   // Barrier that publishes the previous phase's shared-memory writes and the
@@ -529,14 +543,14 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
     cp_async_wait_all();
     group_sync();
     PROF_MARK(0);
-    if (nstep < L) {
+    if (nstep < WL()) {
       const long ns = slot_of(nstep, nr);
       if (ns != cur_slot) issue(nxt, ns);
     }
     return cur;
   };
   auto end_occ = [&](int nstep, int nr) {
-    if (nstep < L) {
+    if (nstep < WL()) {
       const long ns = slot_of(nstep, nr);
       if (ns != cur_slot) {
         double2* t = cur;
@@ -578,12 +592,28 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
   rebuild_sum();
   __syncthreads();
   PROF_MARK(7);
+  // one pass over the current window (run_window, proposed.cpp:275-289);
+  // failures set code / fail_step (step numbers offset by step_off)
+  // Windows (run_window, proposed.cpp:275-289): with a bulk period, one bulk
+  // period after another (compute_bulk_reflection_proposed, proposed.cpp:
+  // 311-342) until R settles, then the slab from the seeded state; each window
+  // ends with extract_reflection (proposed.cpp:204-208). One inline loop: the
+  // window, extraction and bulk logic stay in registers (no outlined calls).
+  long period = 0;
+  double* const Rr = BULK ? p.bulk_scratch + pair * 2 * NP * NP : nullptr;  // previous R
+  double* const Ri = BULK ? Rr + NP * NP : nullptr;
+  for (;;) {
+  const bool main = !bulk_phase;
+  const int L = WL();
+  const int step_off = (int)(period * L);
+  cur_slot = slot_of(0, 0);
+  issue(cur, cur_slot);
   for (int step = 0; step < L; ++step) {
     if constexpr (RK4) {
       // ---------------- classical RK4 (proposed.cpp:141-168), restructured:
       // Qnew = Q + hP + h^2/6 (K1+K2+K3), Pnew = P + h/6 (K1 + 2K2 + 2K3 + K4),
       // X2 = Q + h/2 P, X3 = X2 + h^2/4 K1, X4 = Q + hP + h^2/2 K2, K = -(U+G^2) X
-      const double h = p.h;
+      const double h = wh();
       double *Qr = Xr[0], *Qi = Xi[0], *Yr = Xr[1], *Yi = Xi[1], *Zr = Xr[2], *Zi = Xi[2];
       FOR_BLK {  // Y = X2 = Q + h/2 P
         double v[4];
@@ -643,25 +673,29 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
       // Y = X4 = Qbase + h^2/2 K2; Q = Qbase + h^2/6 (K1 + K2), with
       // h^2/6 K1 = 2/3 (X3 - X2) read back from the planes (no K-sum registers;
       // the rounding is one ulp of |X3|, the size of the Q update's own)
-      if constexpr (SQR) FOR_BLK {
-        double qb[4];
-        own.ld(Qr, Qi, mb, nb, qb);
+      // (braces matter: a _Pragma directly under an if/else is not a safe body)
+      if constexpr (SQR) {
+        FOR_BLK {
+          double qb[4];
+          own.ld(Qr, Qi, mb, nb, qb);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) qb[q] += (0.5 * h * h) * acc[mb][nb][q];
-        own.st(Yr, Yi, mb, nb, qb);
-      }
-      else FOR_BLK {
-        double qb[4], x2[4], x3[4], x4[4];
-        own.ld(Qr, Qi, mb, nb, qb);
-        own.ld(Yr, Yi, mb, nb, x2);
-        own.ld(Zr, Zi, mb, nb, x3);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          x4[q] = qb[q] + (0.5 * h * h) * acc[mb][nb][q];
-          qb[q] += (h * h / 6.0) * acc[mb][nb][q] + (2.0 / 3.0) * (x3[q] - x2[q]);
+          for (int q = 0; q < 4; ++q) qb[q] += (0.5 * h * h) * acc[mb][nb][q];
+          own.st(Yr, Yi, mb, nb, qb);
         }
-        own.st(Yr, Yi, mb, nb, x4);
-        own.st(Qr, Qi, mb, nb, qb);
+      } else {
+        FOR_BLK {
+          double qb[4], x2[4], x3[4], x4[4];
+          own.ld(Qr, Qi, mb, nb, qb);
+          own.ld(Yr, Yi, mb, nb, x2);
+          own.ld(Zr, Zi, mb, nb, x3);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            x4[q] = qb[q] + (0.5 * h * h) * acc[mb][nb][q];
+            qb[q] += (h * h / 6.0) * acc[mb][nb][q] + (2.0 / 3.0) * (x3[q] - x2[q]);
+          }
+          own.st(Yr, Yi, mb, nb, x4);
+          own.st(Qr, Qi, mb, nb, qb);
+        }
       }
       // stage 3 (mid) on X3 (Z)
       box = begin_occ(step, 3);
@@ -718,19 +752,19 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
       if (fsal && step > 0) {
         // kick 0 of this step was merged into the previous step's last kick
         // (same node height); its drift still runs.
-        drift_swap(odrift[0]);
+        drift_swap(wdrift(0));
         r0 = 1;
       }
       for (int r = r0; r < nocc; ++r) {
         const bool last = (r == nocc - 1);
         const int nstep = last ? step + 1 : step;
         const int nr = last ? (fsal ? 1 : 0) : r + 1;
-        if (p.variant == 0) drift_swap(odrift[r]);  // ABA: drift before kick r
+        if (p.variant == 0) drift_swap(wdrift(r));  // ABA: drift before kick r
         double2* box = begin_occ(nstep, nr);
         gemm_box<C, XS>(acc, box, soff, raddr, Ar, Ai, own.col0, lane, kmax, As);
         PROF_MARK(1);
         end_occ(nstep, nr);
-        const double kc = (fsal && last && step + 1 < L) ? p.fsal_kick : okick[r];
+        const double kc = (fsal && last && step + 1 < L) ? wfsal() : wkick(r);
         FOR_BLK {
           double q0[4];
           own.ld(Ar, Ai, mb, nb, q0);
@@ -738,9 +772,9 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
 #pragma unroll
           for (int q = 0; q < 4; ++q) P[mb][nb][q] -= kc * (acc[mb][nb][q] + g2 * q0[q]);
         }
-        if (p.variant == 1 && !last) drift_swap(odrift[r]);  // BAB: drift after kick r
+        if (p.variant == 1 && !last) drift_swap(wdrift(r));  // BAB: drift after kick r
       }
-      if (p.variant == 0) drift_swap(p.final_drift);  // ABA trailing drift
+      if (p.variant == 0) drift_swap(wfin());  // ABA trailing drift
     }
 
     // ---------------- end of step: finite check, Gershgorin, RHST
@@ -752,7 +786,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
     PROF_MARK(4);
     if (xi < 0.0) {
       code = 1;
-      fail_step = step;
+      fail_step = step_off + step;
       break;
     }
     if (xi > p.threshold) {
@@ -788,7 +822,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
                             warp, lane);
       if (!ok) {
         code = 2;
-        fail_step = step;
+        fail_step = step_off + step;
         break;
       }
       own.load(Sr, Si, P);
@@ -796,19 +830,24 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
       set_identity<C>(Ar, Ai, n, tid);
       __syncthreads();
       rebuild_sum();
-      ++rhst;
-      if (!isfinite(xi)) ++npiv;
+      if (main) {  // SolveStats counts the slab solve only (proposed.cpp:328)
+        ++rhst;
+        if (!isfinite(xi)) ++npiv;
+      }
       __syncthreads();
     }
     PROF_MARK(5);
   }
   cp_async_wait_all();
   __syncthreads();
+  if (code) break;
 
-  // ---------------- surface solve: X = R T^-1 (proposed.cpp:204-208), rho = X[:,0]
-  if (code == 0) {
-    double* Sr = RK4 ? Xr[1] : Nr;
-    double* Si = RK4 ? Xi[1] : Ni;
+  // ---------------- extract_reflection (proposed.cpp:204-208): X = R T^-1
+  // with T = G Q - i P, R = G Q + i P; X lands in (Er, Ei). In the bulk phase
+  // the state Q is put back afterwards (the next period continues from it).
+  double* const Er = RK4 ? Xr[1] : Nr;
+  double* const Ei = RK4 ? Xi[1] : Ni;
+  {
     double* Or = Xr[2];  // saved Q: T and R are rebuilt bit-identically for the residual gate
     double* Oi = Xi[2];
     // T = G Q - i P, R = G Q + i P  (i*P = (-pi, pr)), own elements
@@ -833,10 +872,10 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
       tr(mb, nb, q0, t, rr);
       own.st(Or, Oi, mb, nb, q0);
       own.st(Ar, Ai, mb, nb, t);
-      own.st(Sr, Si, mb, nb, rr);
+      own.st(Er, Ei, mb, nb, rr);
     }
     __syncthreads();
-    bool ok = gauss_jordan<C, RK4 ? 4 : 0>(Ar, Ai, Sr, Si, fv, n, *sc, warp, lane);
+    bool ok = gauss_jordan<C, RK4 ? 4 : 0>(Ar, Ai, Er, Ei, fv, n, *sc, warp, lane);
     if (ok && p.residual_check) {
       FOR_BLK {  // A <- T0 (the solver destroyed it)
         double q0[4], t[4], rr[4];
@@ -846,7 +885,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
       }
       __syncthreads();
       ok = residual_ok<C>(
-          Ar, Ai, Sr, Si,
+          Ar, Ai, Er, Ei,
           [&](int mb, int nb, int q) {
             double q0[4], t[4], rr[4];
             own.ld(Or, Oi, mb, nb, q0);
@@ -856,21 +895,103 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
           acc, own, n, *sc, warp, lane);
     }
     if (!ok) {
-      code = 3;
-      fail_step = L;
-    } else {
-      // intensity (curve.cpp:8-20)
-      const double s0 = p.sin_theta0[pair];
-      const double g0 = p.gdiag[pair * n].x;
-      for (int i = tid; i < n; i += C::NT) {
-        const int o = sw<NP>(i, 0);
-        const double2 rho = make_double2(Sr[o], Si[o]);
-        const double2 gi = p.gdiag[pair * n + i];
-        const bool prop = gi.y == 0.0;  // geometry.cpp:46-50: propagating rods have real Gamma
-        p.rho[pair * n + i] = rho;
-        p.eta[pair * n + i] = prop ? (rho.x * rho.x + rho.y * rho.y) * s0 * g0 / gi.x : 0.0;
-      }
+      code = bulk_phase ? 4 : 3;  // "bulk reflection read: ..." / "reflection extraction: ..."
+      fail_step = bulk_phase ? (int)period : L;
+      break;
     }
+    if (BULK && bulk_phase) {
+      FOR_BLK {
+        double q0[4];
+        own.ld(Or, Oi, mb, nb, q0);
+        own.st(Ar, Ai, mb, nb, q0);
+      }
+      __syncthreads();
+      rebuild_sum();
+      __syncthreads();
+    }
+  }
+  if (!(BULK && bulk_phase)) {
+    // intensity (curve.cpp:8-20)
+    const double s0 = p.sin_theta0[pair];
+    const double g0 = p.gdiag[pair * n].x;
+    for (int i = tid; i < n; i += C::NT) {
+      const int o = sw<NP>(i, 0);
+      const double2 rho = make_double2(Er[o], Ei[o]);
+      const double2 gi = p.gdiag[pair * n + i];
+      const bool prop = gi.y == 0.0;  // geometry.cpp:46-50: propagating rods have real Gamma
+      p.rho[pair * n + i] = rho;
+      p.eta[pair * n + i] = prop ? (rho.x * rho.x + rho.y * rho.y) * s0 * g0 / gi.x : 0.0;
+    }
+    break;
+  }
+  if constexpr (BULK) {
+  // ---- bulk: ||R - R_prev||_F <= tol max(1, ||R||_F) (proposed.cpp:334-339)
+  {
+    double dn = 0.0, rn = 0.0;
+    FOR_BLK {
+      double x[4];
+      own.ld(Er, Ei, mb, nb, x);
+      const int o = own.r(mb) * NP + own.c(nb);
+      const double2 pr = *reinterpret_cast<const double2*>(Rr + o);
+      const double2 pi = *reinterpret_cast<const double2*>(Ri + o);
+      if (period > 0) {
+        const double d0 = x[0] - pr.x, d1 = x[1] - pr.y, d2 = x[2] - pi.x, d3 = x[3] - pi.y;
+        dn += d0 * d0 + d1 * d1 + d2 * d2 + d3 * d3;
+      }
+      rn += x[0] * x[0] + x[1] * x[1] + x[2] * x[2] + x[3] * x[3];
+      *reinterpret_cast<double2*>(Rr + o) = make_double2(x[0], x[1]);
+      *reinterpret_cast<double2*>(Ri + o) = make_double2(x[2], x[3]);
+    }
+    dn = warp_sum(dn);
+    rn = warp_sum(rn);
+    if (lane == 0) {
+      sc->red_a[warp] = dn;
+      sc->red_b[warp] = rn;
+    }
+    __syncthreads();
+    double D = 0.0, Rn = 0.0;
+#pragma unroll
+    for (int w = 0; w < C::NW; ++w) {
+      D += sc->red_a[w];
+      Rn += sc->red_b[w];
+    }
+    __syncthreads();
+    if (!(period > 0 && sqrt(D) <= p.bulk_tol * fmax(1.0, sqrt(Rn)))) {
+      if (++period >= p.bulk_max_periods) {
+        code = 5;  // ConvergenceError: the bulk R did not settle
+        fail_step = (int)period;
+        break;
+      }
+      continue;
+    }
+  }
+  // ---- seeded slab: Q = G^-1 (I + R) / 2, P = (i/2)(I - R) (proposed.cpp:114-128)
+  FOR_BLK {
+    const int r = own.r(mb);
+    const double2 gi = r < n ? p.ginv[pair * n + r] : make_double2(0.0, 0.0);
+    const int o = r * NP + own.c(nb);
+    const double2 rr = *reinterpret_cast<const double2*>(Rr + o);
+    const double2 ri = *reinterpret_cast<const double2*>(Ri + o);
+    double q0[4];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int c = own.c(nb) + e;
+      const double dlt = (r == c && r < n) ? 1.0 : 0.0;
+      const double re = (e ? rr.y : rr.x), im = (e ? ri.y : ri.x);
+      const double ar = 0.5 * (dlt + re), ai = 0.5 * im;  // (I + R) / 2
+      q0[e] = gi.x * ar - gi.y * ai;
+      q0[2 + e] = gi.x * ai + gi.y * ar;
+      P[mb][nb][e] = 0.5 * im;  // (i/2)(I - R) = Im(R)/2 + i (1 - Re R)/2
+      P[mb][nb][2 + e] = 0.5 * (dlt - re);
+    }
+    own.st(Ar, Ai, mb, nb, q0);
+  }
+  __syncthreads();
+  rebuild_sum();
+  __syncthreads();
+  bulk_phase = false;
+  period = 0;
+  }
   }
   PROF_MARK(6);
 #ifdef MB_PROFILE
@@ -897,7 +1018,7 @@ static size_t smem_bytes(const PropagateParams& p) {
   b += (size_t)np * sizeof(double);                   // g2s (rsum/dsum alias fv)
   b += (size_t)np * sizeof(int);                      // soff
   b += sizeof(Scratch) + sizeof(PanelScratch) + 16;
-  b += (size_t)kMaxOcc * (2 * sizeof(double) + sizeof(int));  // stepper tables
+  b += (size_t)kMaxOcc * (4 * sizeof(double) + sizeof(int));  // stepper tables (main, bulk)
   b += (size_t)p.ndiff * sizeof(int);
   return b;
 }
@@ -905,10 +1026,10 @@ static size_t smem_bytes(const PropagateParams& p) {
 template <class C, bool RK4>
 static cudaError_t launch_cfg(const PropagateParams& p, cudaStream_t st) {
   const size_t smem = smem_bytes<C, RK4>(p);
-  cudaError_t e = cudaFuncSetAttribute(propagate_kernel<C, RK4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+  auto kern = p.bulk_steps > 0 ? propagate_kernel<C, RK4, true> : propagate_kernel<C, RK4, false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  propagate_kernel<C, RK4><<<(unsigned)p.npairs, C::NT, smem, st>>>(p);
+  kern<<<(unsigned)p.npairs, C::NT, smem, st>>>(p);
   return cudaGetLastError();
 }
 

@@ -16,7 +16,7 @@ def oracle_lattice(o, w):
 def oracle_fields(o, w):
     ff_a, ff_b = configs.form_factors()
     return [o.PotentialField.atoms(w.z_bottom, s.xyz, s.species.astype(np.int32), s.B, ff_a, ff_b, w.cell_area,
-                                   w.gamma_L, w.sign, w.absorption) for s in w.structures]
+                                   w.gamma_L, w.sign, w.absorption, bulk_period=w.bulk_period) for s in w.structures]
 
 
 def run_oracle(o, w, threads=0, method=None, slices=None, threshold=1000.0):
@@ -27,6 +27,7 @@ def run_oracle(o, w, threads=0, method=None, slices=None, threshold=1000.0):
     opts = o.SweepOptions()
     opts.method = method or w.method
     opts.slices = slices or w.slices
+    opts.dz = -w.z_bottom / opts.slices  # the bulk window's target step (sweep.cpp:97-102)
     opts.threads = threads
     opts.rhst_threshold = threshold
     grid = o.AngleGrid.validated(list(w.theta0), list(w.theta1))
@@ -41,7 +42,8 @@ def run_oracle(o, w, threads=0, method=None, slices=None, threshold=1000.0):
 
 def run_device(w, method=None, slices=None, threshold=1000.0, residual_check=True, fsal=False, path=0):
     rods = mb.RodSet.build_first(mb.Lattice2D(w.a1, w.a2), w.n_rods)
-    opts = mb.SweepOptions(method=method or w.method, slices=slices or w.slices, rhst_threshold=threshold,
+    opts = mb.SweepOptions(method=method or w.method, slices=slices or w.slices, dz=-w.z_bottom / (slices or w.slices),
+                           rhst_threshold=threshold,
                            residual_check=residual_check, fsal=fsal, path=path)
     pairs = [(s, t0, t1) for s in range(len(w.structures)) for t1 in w.theta1 for t0 in w.theta0]
     return mb.solve_batch(configs.product_fields(w), rods, w.gamma, pairs, opts)

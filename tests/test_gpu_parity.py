@@ -266,3 +266,51 @@ def test_cluster_matches_batched(n, method):
     assert (sa["code"] == 0).all() and (sb["code"] == 0).all()
     assert np.array_equal(sa["rhst"], sb["rhst"])
     assert H.curve_err(a, b) <= 1e-9
+
+
+# ---------------------------------------------------------------- bulk seed
+def test_bulk_fresnel_interface():  # test_proposed.cpp:281-298 through the device path
+    """A constant potential continued periodically below z_bottom is a
+    semi-infinite medium: the seeded solve gives the Fresnel interface r."""
+    gamma, theta0, u0 = 2.0, 30.0, complex(-0.6, -0.3)
+    g = gamma * math.sin(math.radians(theta0))
+    exp = F.fresnel_interface_r(g, u0)
+    field = mb.PotentialField.tabulated(-2.0, [-2.0, 0.0], [((0, 0), [u0, u0])], bulk_period=1.0)
+    c = mb.rocking_curve(field, dev_rods1(), gamma, mb.AngleGrid.validated([theta0], [0.0]),
+                         mb.SweepOptions(method="sp6", dz=0.01))
+    assert abs(c.rho[0, 0] - exp) <= 1e-8 * abs(exp)
+
+
+@pytest.mark.parametrize("method", ["rk4", "sp4", "sp6"])
+def test_bulk_layered_parity(oracle, method):
+    t0 = [2.0, 7.0, 15.0]
+    of = oracle.PotentialField.gaussian_layers(-10.0, F.LAYERED_LAYERS, 5.0)
+    ref = oracle_curve(oracle, of, F.rods11(oracle), F.K_GAMMA11, t0, method, 0.05)
+    field = mb.PotentialField.gaussian_layers(-10.0, F.LAYERED_LAYERS, bulk_period=5.0)
+    c = mb.rocking_curve(field, dev_rods11(), F.K_GAMMA11, mb.AngleGrid.validated(t0, [0.0]),
+                         mb.SweepOptions(method=method, dz=0.05))
+    assert np.array_equal(c.status["rhst"], ref.rhst)
+    assert H.curve_err(c.eta, ref.eta) <= TOL
+    # R_bulk is defined only to the stopping rule ||dR||_F <= 1e-12 max(1, ||R||_F)
+    # (proposed.cpp:334-339): entries 1e-5 below max eta carry that as ~1e-8
+    assert H.entry_rel_err(c.eta, ref.eta) <= 1e-8
+    assert H.entry_abs_err(c.eta, ref.eta) <= 1e-11
+
+
+@pytest.mark.parametrize("method", ["rk4", "sp6"])
+def test_bulk_atoms_parity(oracle, method):
+    w = configs.config0().subset(theta0=[0.7, 2.1, 4.5, 6.1])
+    w.bulk_period = 3.13  # one 0.78 + 2.35 A layer pair, continued below z_bottom
+    ref, _, rh = H.run_oracle(oracle, w, threads=4, method=method)
+    eta, _, st = H.run_device(w, method=method)
+    assert (st["code"] == 0).all()
+    assert np.array_equal(st["rhst"], rh)
+    assert H.curve_err(eta, ref) <= TOL
+    assert H.entry_rel_err(eta, ref) <= TOL
+
+
+def test_bulk_rejected_off_resident():
+    w = configs.config4(127, "sp6", n_structures=1).subset(theta0=[1.0], slices=10, z_bottom=-0.16)
+    w.bulk_period = 0.1
+    with pytest.raises(mb.ConfigError):
+        H.run_device(w)
