@@ -21,6 +21,7 @@
 #include <complex>
 #include <limits>
 #include <memory>
+#include <optional>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -111,16 +112,21 @@ struct GaussianLayer {
 // potential.hpp:35-61 (+ atoms extension)
 class PotentialField {
  public:
-  static PotentialField zero(double z_bottom) {
+  // bulk_period: the structure repeats below z_bottom with this period; the
+  // solve is then seeded with the bulk reflection (compute_bulk_reflection_proposed)
+  static PotentialField zero(double z_bottom, std::optional<double> bulk_period = {}) {
     PotentialField f;
     f.f_.kind = MB_FIELD_ZERO;
     f.f_.z_bottom = z_bottom;
+    f.set_bulk(bulk_period);
     return f;
   }
-  static PotentialField gaussian_layers(double z_bottom, const std::vector<GaussianLayer>& layers) {
+  static PotentialField gaussian_layers(double z_bottom, const std::vector<GaussianLayer>& layers,
+                                        std::optional<double> bulk_period = {}) {
     PotentialField f;
     f.f_.kind = MB_FIELD_GAUSSIAN_LAYERS;
     f.f_.z_bottom = z_bottom;
+    f.set_bulk(bulk_period);
     for (const GaussianLayer& l : layers)
       f.d0_.insert(f.d0_.end(), {l.z_center, l.amplitude, l.sigma_xy, l.sigma_z, l.absorption});
     f.f_.nlayers = (int)layers.size();
@@ -128,10 +134,12 @@ class PotentialField {
   }
   // entries: (dm, values per grid point)
   static PotentialField tabulated(double z_bottom, const std::vector<double>& z_grid,
-                                  const std::vector<std::pair<std::array<int, 2>, std::vector<Complex>>>& entries) {
+                                  const std::vector<std::pair<std::array<int, 2>, std::vector<Complex>>>& entries,
+                                  std::optional<double> bulk_period = {}) {
     PotentialField f;
     f.f_.kind = MB_FIELD_TABULATED;
     f.f_.z_bottom = z_bottom;
+    f.set_bulk(bulk_period);
     f.d0_ = z_grid;
     for (const auto& e : entries) {
       f.i0_.push_back(e.first[0]);
@@ -154,10 +162,12 @@ class PotentialField {
   static PotentialField atoms(double z_bottom, const std::vector<Atom>& atoms,
                               const std::vector<std::array<double, 4>>& ff_a,
                               const std::vector<std::array<double, 4>>& ff_b, double cell_area, double gamma_L,
-                              double particle_sign, double absorption = 0.1) {
+                              double particle_sign, double absorption = 0.1,
+                              std::optional<double> bulk_period = {}) {
     PotentialField f;
     f.f_.kind = MB_FIELD_ATOMS;
     f.f_.z_bottom = z_bottom;
+    f.set_bulk(bulk_period);
     for (const Atom& a : atoms) {
       f.d0_.insert(f.d0_.end(), {a.x, a.y, a.z});
       f.i0_.push_back(a.species);
@@ -176,6 +186,9 @@ class PotentialField {
     return f;
   }
   double z_bottom() const { return f_.z_bottom; }
+  std::optional<double> bulk_period() const {
+    return f_.has_bulk_period ? std::optional<double>(f_.bulk_period) : std::nullopt;
+  }
   // C view; pointers refer to this object's storage
   mb_field view() const {
     mb_field v = f_;
@@ -202,6 +215,10 @@ class PotentialField {
   }
 
  private:
+  void set_bulk(std::optional<double> p) {
+    f_.has_bulk_period = p ? 1 : 0;
+    f_.bulk_period = p ? *p : 0.0;
+  }
   mb_field f_{};
   std::vector<double> d0_, d1_, d2_, d3_;
   std::vector<int> i0_;
