@@ -20,8 +20,14 @@
 #include <cmath>
 #include <complex>
 #include <limits>
+#include <algorithm>
+#include <charconv>
+#include <cstdio>
+#include <fstream>
+#include <istream>
 #include <memory>
 #include <optional>
+#include <ostream>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -45,6 +51,7 @@ struct BreakdownError : SolverError {
 struct ConvergenceError : SolverError { using SolverError::SolverError; };
 struct DomainError : SolverError { using SolverError::SolverError; };
 struct CompareError : Error { using Error::Error; };
+struct IoError : Error { using Error::Error; };
 struct DeviceError : Error { using Error::Error; };
 
 inline void check(int rc, std::size_t step = 0) {
@@ -258,6 +265,7 @@ struct RockingCurve {
   std::vector<double> eta;  // rows x rods, row-major
   std::vector<Complex> rho;
   std::vector<mb_point_status> status;
+  std::vector<std::string> rod_labels;  // "(m1;m2)" per rod (sweep.cpp:77-80)
   int rods = 0;
   std::string method;
   double dz = 0.0, rhst_threshold = 0.0;
@@ -303,6 +311,8 @@ inline RockingCurve rocking_curve(const PotentialField& field, const RodSet& rod
   c.method = opts.method;
   c.dz = opts.dz;
   c.rhst_threshold = opts.rhst_threshold;
+  for (int i = 0; i < rods.size(); ++i)
+    c.rod_labels.push_back("(" + std::to_string(rods.m(i)[0]) + ";" + std::to_string(rods.m(i)[1]) + ")");
   const mb_field f = field.view();
   const mb_rods r = rods.view();
   const int rc = mb_rocking_curve(context(opts.device), &f, &r, gamma, grid.theta0.data(), (int)grid.theta0.size(),
@@ -339,6 +349,111 @@ inline double curve_error(const RockingCurve& cand, const RockingCurve& ref) {
   if (num == 0.0) return 0.0;
   if (den == 0.0) return std::numeric_limits<double>::infinity();
   return num / den;
+}
+
+
+// ---- curve CSV: the reference's wire format (csvio.cpp:65-149, SURVEY §8f
+// row 2): "# key: value" metadata, header theta0,theta1,eta(m1;m2)..., every
+// number as %.14E, byte-deterministic for a given curve.
+inline std::string format_full(double v) {
+  char buf[40];
+  std::snprintf(buf, sizeof buf, "%.14E", v);
+  std::string s(buf);
+  std::replace(s.begin(), s.end(), ',', '.');  // an embedding app's locale must not leak in
+  return s;
+}
+
+inline void write_curve_csv(std::ostream& os, const RockingCurve& c) {
+  os << "# manybeam-curve v1\n# method: " << c.method << "\n# dz: " << format_full(c.dz) << "\n";
+  if (c.method != "conventional")
+    os << "# rhst_threshold: " << (std::isinf(c.rhst_threshold) ? std::string("inf") : format_full(c.rhst_threshold))
+       << "\n";
+  os << "# rods: " << c.rods << "\ntheta0,theta1";
+  for (const std::string& l : c.rod_labels) os << ",eta" << l;
+  os << "\n";
+  for (long r = 0; r < c.rows(); ++r) {
+    os << format_full(c.theta0[(std::size_t)r]) << ',' << format_full(c.theta1[(std::size_t)r]);
+    for (int i = 0; i < c.rods; ++i) os << ',' << format_full(c.eta_at(r, i));
+    os << "\n";
+  }
+}
+
+inline void write_curve_csv(const std::string& path, const RockingCurve& c) {
+  std::ofstream os(path, std::ios::binary);
+  if (!os) throw IoError("cannot open '" + path + "' for writing");
+  write_curve_csv(os, c);
+  os.flush();
+  if (!os) throw IoError("write to '" + path + "' failed");
+}
+
+inline RockingCurve read_curve_csv(std::istream& is) {
+  auto trim = [](const std::string& x) {
+    const std::size_t a = x.find_first_not_of(" \t\r\n");
+    if (a == std::string::npos) return std::string();
+    return x.substr(a, x.find_last_not_of(" \t\r\n") - a + 1);
+  };
+  auto number = [](const std::string& f, const char* what) {
+    if (f == "inf") return std::numeric_limits<double>::infinity();
+    double v = 0.0;
+    const auto [ptr, ec] = std::from_chars(f.data(), f.data() + f.size(), v, std::chars_format::general);
+    if (ec != std::errc() || ptr != f.data() + f.size())
+      throw IoError(std::string("curve csv: bad ") + what + " value '" + f + "'");
+    return v;
+  };
+  RockingCurve c;
+  std::string line;
+  std::size_t ncols = 0;
+  while (std::getline(is, line)) {
+    const std::string t = trim(line);
+    if (t.empty()) continue;
+    if (t[0] == '#') {
+      const std::size_t colon = t.find(':');
+      if (colon == std::string::npos) continue;
+      const std::string key = trim(t.substr(1, colon - 1)), val = trim(t.substr(colon + 1));
+      if (key == "method") c.method = val;
+      if (key == "dz") c.dz = number(val, "dz");
+      if (key == "rhst_threshold") c.rhst_threshold = number(val, "threshold");
+      continue;
+    }
+    std::vector<std::string> fields;
+    for (std::size_t a = 0;;) {
+      const std::size_t b = t.find(',', a);
+      fields.push_back(trim(t.substr(a, b == std::string::npos ? std::string::npos : b - a)));
+      if (b == std::string::npos) break;
+      a = b + 1;
+    }
+    if (ncols == 0) {
+      if (fields.size() < 3 || fields[0] != "theta0" || fields[1] != "theta1")
+        throw IoError("curve csv: expected header starting with theta0,theta1");
+      for (std::size_t i = 2; i < fields.size(); ++i) {
+        if (fields[i].rfind("eta", 0) != 0) throw IoError("curve csv: intensity columns must be named eta(...)");
+        c.rod_labels.push_back(fields[i].substr(3));
+      }
+      ncols = fields.size();
+      continue;
+    }
+    if (fields.size() != ncols)
+      throw IoError("curve csv: row has " + std::to_string(fields.size()) + " fields, expected " +
+                    std::to_string(ncols));
+    c.theta0.push_back(number(fields[0], "theta0"));
+    c.theta1.push_back(number(fields[1], "theta1"));
+    for (std::size_t i = 2; i < ncols; ++i) c.eta.push_back(number(fields[i], "eta"));
+  }
+  if (ncols == 0) throw IoError("curve csv: missing header row");
+  if (c.theta0.empty()) throw IoError("curve csv: no data rows");
+  c.rods = (int)ncols - 2;
+  return c;
+}
+
+inline RockingCurve read_curve_csv(const std::string& path) {
+  std::ifstream is(path, std::ios::binary);
+  if (!is) throw IoError("cannot open '" + path + "'");
+  return read_curve_csv(is);
+}
+
+// the CLI's `compare a.csv b.csv` (main.cpp): curve_error of two stored curves
+inline double compare_curve_files(const std::string& candidate, const std::string& reference) {
+  return curve_error(read_curve_csv(candidate), read_curve_csv(reference));
 }
 
 }  // namespace manybeam::b200

@@ -63,6 +63,10 @@ class DomainError(SolverError):
     pass
 
 
+class IoError(Error):
+    """types.hpp IoError: curve CSV read/write failures."""
+
+
 class CompareError(Error):
     pass
 
@@ -607,3 +611,78 @@ def device_available(device=0):
         return bool(lib().mb_device_ok(int(device)))
     except Exception:
         return False
+
+# ---------------------------------------------------------------- curve CSV
+# The reference's wire format (csvio.cpp:65-149):
+# "# key: value" metadata, header theta0,theta1,eta(m1;m2)..., every number
+# as %.14E; byte-identical to the C++ writer in include/manybeam_b200.hpp.
+def format_full(v):
+    return ("%.14E" % float(v)).replace(",", ".")
+
+
+def write_curve_csv(path, curve):
+    lines = ["# manybeam-curve v1", f"# method: {curve.method}", f"# dz: {format_full(curve.dz)}"]
+    if curve.method != "conventional":
+        thr = curve.rhst_threshold
+        lines.append("# rhst_threshold: " + ("inf" if math.isinf(thr) else format_full(thr)))
+    eta = np.asarray(curve.eta)
+    lines.append(f"# rods: {eta.shape[1]}")
+    lines.append(",".join(["theta0", "theta1"] + [f"eta{l}" for l in curve.rod_labels]))
+    for r in range(eta.shape[0]):
+        lines.append(",".join([format_full(curve.theta0[r]), format_full(curve.theta1[r])] +
+                              [format_full(x) for x in eta[r]]))
+    try:
+        with open(path, "wb") as f:
+            f.write(("\n".join(lines) + "\n").encode())
+    except OSError as e:
+        raise IoError(f"cannot open '{path}' for writing") from e
+
+
+def read_curve_csv(path):
+    try:
+        text = open(path, "rb").read().decode()
+    except OSError as e:
+        raise IoError(f"cannot open '{path}'") from e
+    meta, labels, t0, t1, rows, ncols = {}, None, [], [], [], 0
+
+    def num(f, what):
+        if f == "inf":
+            return math.inf
+        try:
+            return float(f)
+        except ValueError:
+            raise IoError(f"curve csv: bad {what} value '{f}'") from None
+
+    for line in text.splitlines():
+        t = line.strip()
+        if not t:
+            continue
+        if t.startswith("#"):
+            if ":" in t:
+                k, v = t[1:].split(":", 1)
+                meta[k.strip()] = v.strip()
+            continue
+        fields = [x.strip() for x in t.split(",")]
+        if labels is None:
+            if len(fields) < 3 or fields[0] != "theta0" or fields[1] != "theta1":
+                raise IoError("curve csv: expected header starting with theta0,theta1")
+            if not all(f.startswith("eta") for f in fields[2:]):
+                raise IoError("curve csv: intensity columns must be named eta(...)")
+            labels, ncols = [f[3:] for f in fields[2:]], len(fields)
+            continue
+        if len(fields) != ncols:
+            raise IoError(f"curve csv: row has {len(fields)} fields, expected {ncols}")
+        t0.append(num(fields[0], "theta0"))
+        t1.append(num(fields[1], "theta1"))
+        rows.append([num(f, "eta") for f in fields[2:]])
+    if labels is None:
+        raise IoError("curve csv: missing header row")
+    if not rows:
+        raise IoError("curve csv: no data rows")
+    return RockingCurve(t0, t1, np.array(rows), labels, meta.get("method", ""), num(meta.get("dz", "0"), "dz"),
+                        num(meta.get("rhst_threshold", "inf"), "threshold"))
+
+
+def compare_curve_files(candidate, reference):
+    """The reference CLI's `compare` (main.cpp): curve_error of two stored curves."""
+    return curve_error(read_curve_csv(candidate), read_curve_csv(reference))

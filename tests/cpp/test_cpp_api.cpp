@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <sstream>
 
 #include "../../include/manybeam_b200.hpp"
 
@@ -30,7 +31,39 @@ static int failures = 0;
   } while (0)
 
 int main(int argc, char** argv) {
+  // `--rewrite in.csv out.csv`: read a curve CSV and write it back (byte
+  // round trip against the Python writer, tests/test_cpp_api.py)
+  if (argc == 4 && std::strcmp(argv[1], "--rewrite") == 0) {
+    write_curve_csv(std::string(argv[3]), read_curve_csv(std::string(argv[2])));
+    return 0;
+  }
   const bool device = !(argc > 1 && std::strcmp(argv[1], "--no-device") == 0);
+  {  // csvio.cpp:65-149 wire format
+    RockingCurve c;
+    c.theta0 = {0.5, 1.25};
+    c.theta1 = {0.0, 0.0};
+    c.rods = 2;
+    c.rod_labels = {"(0;0)", "(1;-1)"};
+    c.eta = {0.125, 3.0e-17, 1.0 / 3.0, 0.0};
+    c.method = "sp6";
+    c.dz = 0.01;
+    c.rhst_threshold = std::numeric_limits<double>::infinity();
+    std::ostringstream os;
+    write_curve_csv(os, c);
+    const std::string want =
+        "# manybeam-curve v1\n# method: sp6\n# dz: 1.00000000000000E-02\n# rhst_threshold: inf\n# rods: 2\n"
+        "theta0,theta1,eta(0;0),eta(1;-1)\n"
+        "5.00000000000000E-01,0.00000000000000E+00,1.25000000000000E-01,3.00000000000000E-17\n"
+        "1.25000000000000E+00,0.00000000000000E+00,3.33333333333333E-01,0.00000000000000E+00\n";
+    CHECK(os.str() == want);
+    std::istringstream is(os.str());
+    const RockingCurve back = read_curve_csv(is);
+    CHECK(back.rows() == 2 && back.rods == 2 && back.rod_labels[1] == "(1;-1)" && back.method == "sp6");
+    CHECK(std::isinf(back.rhst_threshold) && back.dz == 0.01);
+    CHECK(curve_error(back, c) <= 1e-15);
+    std::istringstream bad("theta0,theta1,eta(0;0)\n1.0,2.0\n");
+    CHECK_THROWS_AS(read_curve_csv(bad), IoError);
+  }
   // test_rods_geometry.cpp:39-45 : the canonical 11-rod set
   const Lattice2D rect{{2.0, 0.0}, {0.0, 2.6}};
   const RodSet rods = RodSet::build(rect, 5.0);
@@ -62,6 +95,13 @@ int main(int argc, char** argv) {
       worst = std::max(worst, s);
     }
     CHECK(worst <= 1.0 + 1e-8 && worst > 0.0);  // acceptance.cpp:308-319
+    {  // a device curve through the wire format
+      std::ostringstream os;
+      write_curve_csv(os, a);
+      std::istringstream is(os.str());
+      const RockingCurve back = read_curve_csv(is);
+      CHECK(back.rod_labels == a.rod_labels && curve_error(back, a) <= 1e-14);
+    }
     // test_sweep.cpp:90-105: breakdown surfaces with its step
     std::vector<GaussianLayer> deep;
     for (int i = 0; i < 75; ++i) deep.push_back({-1.0 - 2.0 * i, -0.22, 2.2, 0.7, 0.08});
