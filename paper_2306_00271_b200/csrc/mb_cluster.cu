@@ -55,22 +55,32 @@ namespace mbx {
 
 namespace {
 
-constexpr int SW = 16;  // slab columns per CTA = rows per CTA in the solve layout
 constexpr int CNT = 256, CNW = 8;
 constexpr int WCH = 32;  // columns per DSMEM chunk of the blocked solve
 
-template <int NP_>
+// SW = slab columns per CTA = rows per CTA in the solve layout (16 at NP=256,
+// 32 at NP=128: the wider slab gives the warps C64's 16x32 tile)
+template <int NP_, int SW_>
 struct CCfg {
-  static constexpr int NP = NP_;
+  static constexpr int NP = NP_, SW = SW_;
   static constexpr int MB = NP / 64;  // row blocks per warp, interleaved: rb = warp + 8 m
-  static constexpr int NB = 2;        // the slab's two 8-column blocks
+  static constexpr int NB = SW / 8;   // the slab's 8-column blocks
   static constexpr int NQ = NP / 32;  // row entries per lane in the solve layout
-  static constexpr int MINB = 1;  // resident CTAs per SM
+  static constexpr int MINB = 1;      // resident CTAs per SM
+  static constexpr int TPR = CNT / SW;      // threads per row in the row-layout phases
+  static constexpr int SLOTS = 2 * SW / TPR;  // special-column slots per thread
 };
 
-// slab plane [NP rows][16 cols]: the XOR puts rows r and r+1 in opposite bank
-// halves (B fragments: 4 rows x 8 cols; own-element double2 accesses)
-__device__ __forceinline__ int ss(int r, int c) { return r * SW + (c ^ ((r & 1) << 3)); }
+// slab plane [NP rows][SW cols]. SW=16: the XOR puts rows r and r+1 in
+// opposite bank halves; SW=32: rows r..r+3 rotate by 4 doubles. Both keep the
+// B fragments (4 rows x 8 cols) and own-element double2 accesses conflict-free.
+template <int SW>
+__device__ __forceinline__ int ss(int r, int c) {
+  if constexpr (SW == 16)
+    return r * 16 + (c ^ ((r & 1) << 3));
+  else
+    return r * SW + (c ^ ((r & 3) << 2));
+}
 
 struct Layout {
   size_t planes, boxes, fpub, tpub, tloc, wch, scr, g2s, rsum, dsum, pubv, occ, soff, sboxpos, total;
@@ -78,7 +88,7 @@ struct Layout {
 
 __host__ __device__ inline size_t al16(size_t b) { return (b + 15) & ~(size_t)15; }
 
-__host__ __device__ inline Layout cluster_layout(int np, int nq, int box_size, int ndiff) {
+__host__ __device__ inline Layout cluster_layout(int np, int SW, int nq, int box_size, int ndiff) {
   Layout L{};
   size_t o = 0;
   L.planes = o;
@@ -134,7 +144,7 @@ __device__ __forceinline__ void slab_gemm(double (&acc)[C::MB][C::NB][4], const 
     double br[C::NB], bi[C::NB], bs[C::NB];
 #pragma unroll
     for (int nb = 0; nb < C::NB; ++nb) {
-      const int o = ss(k, nb * 8 + cl);
+      const int o = ss<C::SW>(k, nb * 8 + cl);
       br[nb] = Xr[o];
       bi[nb] = Xi[o];
       bs[nb] = br[nb] + bi[nb];
@@ -164,15 +174,15 @@ __device__ __forceinline__ void slab_gemm(double (&acc)[C::MB][C::NB][4], const 
       }
 }
 
-// residual tile configuration (16 rows x NP/8 columns per warp)
-template <int NP_>
+// residual tile configuration (SW rows x NP/8 columns per warp)
+template <int NP_, int SW_>
 struct RCfg {
-  static constexpr int NP = NP_, MB = 2, NB = NP / 64;
+  static constexpr int NP = NP_, MB = SW_ / 8, NB = NP / 64;
 };
 
 template <class C, bool RK4>
 __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_constant__ PropagateParams p) {
-  constexpr int NP = C::NP, MB = C::MB, NB = C::NB, NQ = C::NQ;
+  constexpr int NP = C::NP, MB = C::MB, NB = C::NB, NQ = C::NQ, SW = C::SW, TPR = C::TPR, SLOTS = C::SLOTS;
   constexpr int PL = NP * SW;  // doubles per slab plane
   cg::cluster_group cl = cg::this_cluster();
   const int cs = (int)cl.num_blocks();
@@ -186,7 +196,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
 #endif
 
   extern __shared__ __align__(16) unsigned char smem[];
-  const Layout LY = cluster_layout(NP, RK4 ? 3 : 2, p.box_size, p.ndiff);
+  const Layout LY = cluster_layout(NP, SW, RK4 ? 3 : 2, p.box_size, p.ndiff);
   double* const planes = reinterpret_cast<double*>(smem + LY.planes);
   double2* const boxes = reinterpret_cast<double2*>(smem + LY.boxes);
   double2* const fpub = reinterpret_cast<double2*>(smem + LY.fpub);  // [2][NP] panel multiplier rows
@@ -252,7 +262,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
   auto ocol = [&](int nb) { return 8 * nb + 2 * (lane & 3); };
   auto live = [&](int m) { return 8 * (warp + 8 * m) < n; };
   auto ld = [&](const double* Xr, const double* Xi, int m, int nb, double (&v)[4]) {
-    const int o = ss(orow(m), ocol(nb));
+    const int o = ss<SW>(orow(m), ocol(nb));
     const double2 a = *reinterpret_cast<const double2*>(Xr + o);
     const double2 b = *reinterpret_cast<const double2*>(Xi + o);
     v[0] = a.x;
@@ -261,7 +271,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
     v[3] = b.y;
   };
   auto st = [&](double* Xr, double* Xi, int m, int nb, const double (&v)[4]) {
-    const int o = ss(orow(m), ocol(nb));
+    const int o = ss<SW>(orow(m), ocol(nb));
     *reinterpret_cast<double2*>(Xr + o) = make_double2(v[0], v[1]);
     *reinterpret_cast<double2*>(Xi + o) = make_double2(v[2], v[3]);
   };
@@ -283,8 +293,8 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
       const int i = col0 + c;
       if (i < n) {
         const double2 g = ginv_half ? p.ginv[pair * n + i] : make_double2(2.0, 0.0);
-        Xr[ss(i, c)] = 0.5 * g.x;
-        Xi[ss(i, c)] = 0.5 * g.y;
+        Xr[ss<SW>(i, c)] = 0.5 * g.x;
+        Xi[ss<SW>(i, c)] = 0.5 * g.y;
       }
     }
   };
@@ -464,9 +474,9 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
     double2* fs = tloc + 8 * SW;                                // [16][32] F on special columns
     double2* linv = fs + 2 * SW * SW;                           // [16] 1/pivot
     double* lpv = reinterpret_cast<double*>(linv + SW);         // [16] |pivot|^2
-    // 16 threads per row: lr = tid / 16 (16 rows), slots cg and cg + 16
-    const int lr = tid >> 4, cg = tid & 15, gi = col0 + lr;
-    const int rbase = lane & ~15;
+    // TPR threads per row: lr = tid / TPR (SW rows), slots cg + TPR u
+    const int lr = tid / TPR, cg = tid % TPR, gi = col0 + lr;
+    const int rbase = lane & ~(TPR - 1);
     bool okb = true;
     for (int b = 0; b < npan; ++b) {
       wait_panel(b, sid);
@@ -533,10 +543,10 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
         double* Xi = isA ? Ai_ : Bi_;
         const bool act = gi < n && (isA ? gi >= p0 + SW : true);
         // (A) sequential ops on the special columns
-        double2 val[2];
+        double2 val[SLOTS];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int j = scol[cg + 16 * u];
+        for (int u = 0; u < SLOTS; ++u) {
+          const int j = scol[cg + TPR * u];
           val[u] = (act && j >= 0) ? make_double2(Xr[sw<NP>(lr, j)], Xi[sw<NP>(lr, j)]) : make_double2(0.0, 0.0);
         }
         double2 xk[SW];
@@ -546,17 +556,20 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
           if (lk < nk) {
             const int ps = pslot[lk], ks = lk;
             auto pick = [&](int sl) {
-              const double2 v = (sl >> 4) ? val[1] : val[0];
-              return make_double2(__shfl_sync(0xffffffffu, v.x, rbase | (sl & 15)),
-                                  __shfl_sync(0xffffffffu, v.y, rbase | (sl & 15)));
+              double2 v = val[0];
+#pragma unroll
+              for (int u = 1; u < SLOTS; ++u)
+                if (sl / TPR == u) v = val[u];
+              return make_double2(__shfl_sync(0xffffffffu, v.x, rbase | (sl % TPR)),
+                                  __shfl_sync(0xffffffffu, v.y, rbase | (sl % TPR)));
             };
             const double2 xp = pick(ps);
             const double2 xold = pick(ks);
             const double2 x = cmul(xp, linv[lk]);
             xk[lk] = x;
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
-              const int sl = cg + 16 * u;
+            for (int u = 0; u < SLOTS; ++u) {
+              const int sl = cg + TPR * u;
               const double2 f = fs[lk * 2 * SW + sl];
               const double2 v = (sl == ps) ? xold : val[u];
               const double2 nv = make_double2(v.x - (f.x * x.x - f.y * x.y), v.y - (f.x * x.y + f.y * x.x));
@@ -566,8 +579,8 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
         }
         if (act) {
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int j = scol[cg + 16 * u];
+          for (int u = 0; u < SLOTS; ++u) {
+            const int j = scol[cg + TPR * u];
             if (j >= 0) {
               Xr[sw<NP>(lr, j)] = val[u].x;
               Xi[sw<NP>(lr, j)] = val[u].y;
@@ -577,31 +590,39 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
         // (B) other columns: X[i][j] -= sum_k x_k F_k[j] (F_k[j] = A[k][j]),
         // F chunks from the owner through DSMEM, next chunk prefetched into
         // registers while the current one is applied
-        const int ldt = tid / (WCH / 2), ldj = 2 * (tid % (WCH / 2));  // 16 x 32 chunk, one double2 each
-        auto fetch = [&](int j0, double2& a, double2& c) {
-          const int j = j0 + ldj;
-          a = make_double2(0.0, 0.0);
-          c = a;
-          if (ldt < nk && j < NP) {
-            const long o = (long)ldt * NP + j;
-            a = __ldcg(reinterpret_cast<const double2*>(war + o));
-            c = __ldcg(reinterpret_cast<const double2*>(wai + o));
+        // SW x WCH chunk, FR double2 per thread and plane
+        constexpr int FR = SW * (WCH / 2) / CNT;
+        auto fetch = [&](int j0, double2 (&a)[FR], double2 (&c)[FR]) {
+#pragma unroll
+          for (int f = 0; f < FR; ++f) {
+            const int w = tid + f * CNT, ldt = w / (WCH / 2), j = j0 + 2 * (w % (WCH / 2));
+            a[f] = make_double2(0.0, 0.0);
+            c[f] = a[f];
+            if (ldt < nk && j < NP) {
+              const long o = (long)ldt * NP + j;
+              a[f] = __ldcg(reinterpret_cast<const double2*>(war + o));
+              c[f] = __ldcg(reinterpret_cast<const double2*>(wai + o));
+            }
+            if (j >= n || ((smask[j >> 5] >> (j & 31)) & 1u)) a[f].x = c[f].x = 0.0;
+            if (j + 1 >= n || ((smask[(j + 1) >> 5] >> ((j + 1) & 31)) & 1u)) a[f].y = c[f].y = 0.0;
           }
-          if (j >= n || ((smask[j >> 5] >> (j & 31)) & 1u)) a.x = c.x = 0.0;
-          if (j + 1 >= n || ((smask[(j + 1) >> 5] >> ((j + 1) & 31)) & 1u)) a.y = c.y = 0.0;
         };
-        double2 na, nc;
+        double2 na[FR], nc[FR];
         fetch(0, na, nc);
         for (int j0 = 0; j0 < n; j0 += WCH) {
           __syncthreads();  // previous chunk consumed (and the special write-back done)
-          *reinterpret_cast<double2*>(wchr + ldt * WCH + ldj) = na;
-          *reinterpret_cast<double2*>(wchi + ldt * WCH + ldj) = nc;
+#pragma unroll
+          for (int f = 0; f < FR; ++f) {
+            const int w = tid + f * CNT, ldt = w / (WCH / 2), ldj = 2 * (w % (WCH / 2));
+            *reinterpret_cast<double2*>(wchr + ldt * WCH + ldj) = na[f];
+            *reinterpret_cast<double2*>(wchi + ldt * WCH + ldj) = nc[f];
+          }
           __syncthreads();
           if (j0 + WCH < n) fetch(j0 + WCH, na, nc);
           if (act) {
 #pragma unroll
-            for (int u = 0; u < WCH / 16; ++u) {
-              const int jj = cg + 16 * u, j = j0 + jj;
+            for (int u = 0; u < WCH / TPR; ++u) {
+              const int jj = cg + TPR * u, j = j0 + jj;
               if (j >= n) continue;
               const int o = sw<NP>(lr, j);
               double xr = Xr[o], xi = Xi[o];
@@ -664,7 +685,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
     // residual gate ||X A0 - B0||_F <= 1e-10 ||B0||_F over the cluster
     // (kernels.cpp:73-79): own 16 rows of X times A0 (L2), k-chunks of 16 rows
     // staged into the (now free) A rows area
-    using R = RCfg<NP>;
+    using R = RCfg<NP, SW>;
     double racc[R::MB][R::NB][4];
 #pragma unroll
     for (int a = 0; a < R::MB; ++a)
@@ -973,7 +994,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
       bad = __syncthreads_or(bad);
       if (tid == 0) pubv[4] = bad ? 1.0 : 0.0;
       cl.sync();  // #1: slab partials visible
-      const int lr = tid >> 4, src = tid & 15, i = col0 + lr;
+      const int lr = tid / TPR, src = tid % TPR, i = col0 + lr;  // cs <= TPR
       double Rr = 0.0, Dd = 0.0, Bf = 0.0;
       if (src < cs) {
         if (i < n) {
@@ -983,7 +1004,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
         if (lr == 0) Bf = cl.map_shared_rank(pubv, src)[4];
       }
 #pragma unroll
-      for (int o = 8; o > 0; o >>= 1) {
+      for (int o = TPR / 2; o > 0; o >>= 1) {
         Rr += __shfl_xor_sync(0xffffffffu, Rr, o);
         Dd += __shfl_xor_sync(0xffffffffu, Dd, o);
         Bf = fmax(Bf, __shfl_xor_sync(0xffffffffu, Bf, o));
@@ -994,10 +1015,13 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
         lo = Dd - Rr;
         nd = (Dd - Rr <= 0.0) ? 1.0 : 0.0;
       }
-      hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, 16));
-      lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, 16));
-      nd = fmax(nd, __shfl_xor_sync(0xffffffffu, nd, 16));
-      Bf = fmax(Bf, __shfl_xor_sync(0xffffffffu, Bf, 16));
+#pragma unroll
+      for (int o = TPR; o < 32; o <<= 1) {  // the warp's 32/TPR rows
+        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        nd = fmax(nd, __shfl_xor_sync(0xffffffffu, nd, o));
+        Bf = fmax(Bf, __shfl_xor_sync(0xffffffffu, Bf, o));
+      }
       if (lane == 0) {
         sc->red_a[warp] = hi;
         sc->red_b[warp] = lo;
@@ -1132,7 +1156,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
 
 template <class C, bool RK4>
 cudaError_t launch_cfg(const PropagateParams& p, cudaStream_t st, int cs) {
-  const Layout LY = cluster_layout(C::NP, RK4 ? 3 : 2, p.box_size, p.ndiff);
+  const Layout LY = cluster_layout(C::NP, C::SW, RK4 ? 3 : 2, p.box_size, p.ndiff);
   auto kern = cluster_kernel<C, RK4>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LY.total);
   if (e != cudaSuccess) return e;
@@ -1157,21 +1181,31 @@ cudaError_t launch_cfg(const PropagateParams& p, cudaStream_t st, int cs) {
 
 }  // namespace
 
+// slab width per padded size: NP=256 -> 16 columns (CS <= 16); NP=128 -> 32
+// for splitting (CS <= 4), 16 for rk4 (its third slab plane does not fit at 32)
+#ifndef MB_SW128
+#define MB_SW128 32
+#endif
+static int cluster_sw(int np, int rk4) { return np == 128 && !rk4 ? MB_SW128 : 16; }
+
 size_t cluster_smem_bytes(int n, int rk4, int box_size, int ndiff) {
   if (n <= 64 || n > 256) return 0;
   const int np = n <= 128 ? 128 : 256;
-  return cluster_layout(np, rk4 ? 3 : 2, box_size, ndiff).total;
+  return cluster_layout(np, cluster_sw(np, rk4), rk4 ? 3 : 2, box_size, ndiff).total;
 }
 
 int cluster_np(int n) { return n <= 64 || n > 256 ? 0 : (n <= 128 ? 128 : 256); }
 
 cudaError_t launch_cluster(const PropagateParams& p, cudaStream_t st, int* launches) {
-  const int cs = (p.n + SW - 1) / SW;
   cudaError_t e;
-  if (p.n <= 128)
-    e = p.rk4 ? launch_cfg<CCfg<128>, true>(p, st, cs) : launch_cfg<CCfg<128>, false>(p, st, cs);
-  else
-    e = p.rk4 ? launch_cfg<CCfg<256>, true>(p, st, cs) : launch_cfg<CCfg<256>, false>(p, st, cs);
+  if (p.n <= 128) {
+    constexpr int S = MB_SW128;
+    e = p.rk4 ? launch_cfg<CCfg<128, 16>, true>(p, st, (p.n + 15) / 16)
+              : launch_cfg<CCfg<128, S>, false>(p, st, (p.n + S - 1) / S);
+  } else {
+    const int cs = (p.n + 15) / 16;
+    e = p.rk4 ? launch_cfg<CCfg<256, 16>, true>(p, st, cs) : launch_cfg<CCfg<256, 16>, false>(p, st, cs);
+  }
   if (e == cudaSuccess) ++*launches;
   return e == cudaSuccess ? cudaGetLastError() : e;
 }
