@@ -113,8 +113,8 @@ __host__ __device__ inline Layout cluster_layout(int np, int SW, int nq, int box
   o += al16((size_t)np * sizeof(double));
   L.pubv = o;
   o += al16(8 * sizeof(double));
-  L.occ = o;  // occ_kick, occ_drift (double) then occ_node (int), kMaxOcc each
-  o += al16((size_t)kMaxOcc * (2 * sizeof(double) + sizeof(int)));
+  L.occ = o;  // occ_kick, occ_drift, bulk kick, bulk drift (double) then occ_node (int), kMaxOcc each
+  o += al16((size_t)kMaxOcc * (4 * sizeof(double) + sizeof(int)));
   L.soff = o;
   o += al16((size_t)np * sizeof(int));
   L.sboxpos = o;
@@ -180,7 +180,10 @@ struct RCfg {
   static constexpr int NP = NP_, MB = SW_ / 8, NB = NP / 64;
 };
 
-template <class C, bool RK4>
+// BULK: the bulk-layer seed (compute_bulk_reflection_proposed,
+// proposed.cpp:311-342) runs first, as in the resident kernel; compiled
+// separately so the plain kernels keep their registers.
+template <class C, bool RK4, bool BULK>
 __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_constant__ PropagateParams p) {
   constexpr int NP = C::NP, MB = C::MB, NB = C::NB, NQ = C::NQ, SW = C::SW, TPR = C::TPR, SLOTS = C::SLOTS;
   constexpr int PL = NP * SW;  // doubles per slab plane
@@ -211,7 +214,9 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
   double* const pubv = reinterpret_cast<double*>(smem + LY.pubv);  // [0..3] check, [4] bad, [5..7] residual
   double* const okick = reinterpret_cast<double*>(smem + LY.occ);  // runtime-indexed
   double* const odrift = okick + kMaxOcc;                            // stepper tables in
-  int* const onode = reinterpret_cast<int*>(odrift + kMaxOcc);       // shared memory
+  double* const bkick = odrift + kMaxOcc;                            // shared memory
+  double* const bdrift = bkick + kMaxOcc;                            // (bulk window: h_bulk)
+  int* const onode = reinterpret_cast<int*>(bdrift + kMaxOcc);
   int* const soff = reinterpret_cast<int*>(smem + LY.soff);
   int* const sboxpos = reinterpret_cast<int*>(smem + LY.sboxpos);
   // slab planes: X0, X1 (, X2) re/im
@@ -228,7 +233,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
   double* const Bi_ = planes + 3 * SW * NP;
   // per-pair L2 scratch: M0 (A), M1 (B), row-major NP x NP planes
   const long NN = (long)NP * NP;
-  double* const M0r = p.scratch + pair * 6 * NN;
+  double* const M0r = p.scratch + pair * (BULK ? 8 : 6) * NN;
   double* const M0i = M0r + NN;
   double* const M1r = M0r + 2 * NN;
   double* const M1i = M0r + 3 * NN;
@@ -239,6 +244,9 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
   double* const M2r = M0r + 4 * NN;
   double* const M2i = M0r + 5 * NN;
 
+  // M3: the own Q slab saved across a bulk period's reflection read
+  double* const M3r = M0r + 6 * NN;
+  double* const M3i = M0r + 7 * NN;
   const double2* coef = p.coef + (long)p.pair_struct[pair] * p.nslots * p.ndiff;
   const int kmax = (n + 3) & ~3;
   for (int i = tid; i < p.ndiff; i += CNT) sboxpos[i] = p.boxpos[i];
@@ -246,6 +254,8 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
   for (int i = tid; i < kMaxOcc; i += CNT) {
     okick[i] = p.occ_kick[i];
     odrift[i] = p.occ_drift[i];
+    bkick[i] = BULK ? p.bulk_kick[i] : 0.0;
+    bdrift[i] = BULK ? p.bulk_drift[i] : 0.0;
     onode[i] = p.occ_node[i];
   }
   // box holes are read for the padded k in [n, kmax) (times zero rows of X):
@@ -316,7 +326,13 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
   }
   double acc[MB][NB][4];
 
-  auto slot_of = [&](int step, int r) -> long { return (long)step * p.slot_stride + onode[r]; };
+  // the propagation window: the slab (main) or one bulk period (bulk seeding,
+  // proposed.cpp:311-321: the same stepper on the bulk window's step)
+  bool bulk_phase = BULK && p.bulk_steps > 0;
+  auto wbase = [&]() -> long { return (BULK && bulk_phase) ? p.bulk_base : 0L; };
+  auto wkick = [&](int r) -> double { return (BULK && bulk_phase) ? bkick[r] : okick[r]; };
+  auto wdrift = [&](int r) -> double { return (BULK && bulk_phase) ? bdrift[r] : odrift[r]; };
+  auto slot_of = [&](int step, int r) -> long { return wbase() + (long)step * p.slot_stride + onode[r]; };
   auto issue = [&](double2* dst, long slot) {
     const double2* src = coef + slot * p.ndiff;
     for (int d = tid; d < p.ndiff; d += CNT) cp_async16(dst + sboxpos[d], src + d);
@@ -326,11 +342,11 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
   double2* nxt = boxes + p.box_size;
   __syncthreads();
   CPROF(7);
-  long cur_slot = slot_of(0, 0);
-  issue(cur, cur_slot);
+  long cur_slot = 0;
 
   int rhst = 0, npiv = 0, code = 0, fail_step = 0;
-  const int nocc = p.nocc, L = p.nsteps;
+  const int nocc = p.nocc;
+  int L = p.nsteps;
   const bool fsal = !RK4 && p.fsal && p.variant == 1;
 
   auto begin_occ = [&](int nstep, int nr) -> double2* {
@@ -491,30 +507,31 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
         lpv[tid] = reinterpret_cast<const double*>(rt + SW)[tid];
       }
       __syncthreads();
-      // special columns: the panel's, then pivots outside it (first occurrence)
-      if (tid == 0) {
-        int cnt = SW;
-        bool fail = false;
-        for (int q = 0; q < NP / 32; ++q) smask[q] = 0u;
-        for (int c = 0; c < SW; ++c) {
-          scol[c] = p0 + c;
-          if (p0 + c < NP) smask[(p0 + c) >> 5] |= 1u << ((p0 + c) & 31);
-        }
-        for (int lk = 0; lk < nk; ++lk) {
-          const int pk = lpp[lk];
-          fail |= !(lpv[lk] > 0.0);
-          int sl = (pk >= p0 && pk < p0 + SW) ? pk - p0 : -1;
-          for (int c = SW; sl < 0 && c < cnt; ++c)
-            if (scol[c] == pk) sl = c;
-          if (sl < 0) {
-            sl = cnt;
-            scol[cnt++] = pk;
-            smask[pk >> 5] |= 1u << (pk & 31);
-          }
-          pslot[lk] = sl;
-        }
-        for (int c = cnt; c < 2 * SW; ++c) scol[c] = -1;
-        sn[0] = fail ? -1 : cnt;
+      // special columns: the panel's, then pivots outside it (first occurrence,
+      // in pivot order), built by one warp (lane lk <-> pivot lk; SW <= 32)
+      if (warp == 0) {
+        const unsigned FULL = 0xffffffffu, lower = (1u << lane) - 1u;
+        const bool has = lane < nk;
+        const int pk = has ? lpp[lane] : -1;
+        const bool bad = has && !(lpv[lane] > 0.0);
+        const bool inpan = has && pk >= p0 && pk < p0 + SW;
+        const bool outside = has && !inpan;
+        const unsigned outm = __ballot_sync(FULL, outside);
+        const unsigned same = __match_any_sync(FULL, outside ? pk : -1 - lane) & outm;
+        const bool first = outside && (same & lower) == 0u;
+        const unsigned firstm = __ballot_sync(FULL, first);
+        const int cnt = SW + __popc(firstm);
+        if (inpan) pslot[lane] = pk - p0;
+        if (outside) pslot[lane] = SW + __popc(firstm & ((1u << (__ffs(same) - 1)) - 1u));
+        for (int q = lane; q < NP / 32; q += 32) smask[q] = 0u;
+        if (lane < SW) scol[lane] = p0 + lane;
+        if (first) scol[SW + __popc(firstm & lower)] = pk;
+        for (int c = cnt + lane; c < 2 * SW; c += 32) scol[c] = -1;
+        __syncwarp();
+        if (lane < SW && p0 + lane < NP) atomicOr(&smask[(p0 + lane) >> 5], 1u << ((p0 + lane) & 31));
+        if (first) atomicOr(&smask[pk >> 5], 1u << (pk & 31));
+        const bool anybad = __any_sync(FULL, bad);
+        if (lane == 0) sn[0] = anybad ? -1 : cnt;
       }
       __syncthreads();
       if (sn[0] < 0) {  // zero pivot: the same owner data everywhere
@@ -818,11 +835,28 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
     }
   };
 
+  // Windows (run_window, proposed.cpp:275-289): with a bulk period, one bulk
+  // period after another (compute_bulk_reflection_proposed, proposed.cpp:
+  // 311-342) until R settles, then the slab from the seeded state; each window
+  // ends with extract_reflection (proposed.cpp:204-208).
+  long period = 0;
+  double* const Rr = BULK ? p.bulk_scratch + pair * 2 * NN : nullptr;  // previous R (row-major)
+  double* const Ri = BULK ? Rr + NN : nullptr;
+  bool again = false;  // BULK: another window follows
+  do {
+  again = false;
+  L = (BULK && bulk_phase) ? p.bulk_steps : p.nsteps;
+  const double wh = (BULK && bulk_phase) ? p.bulk_h : p.h;
+  const double wfin = (BULK && bulk_phase) ? p.bulk_final_drift : p.final_drift;
+  const double wfsal = (BULK && bulk_phase) ? p.bulk_fsal_kick : p.fsal_kick;
+  const int step_off = (int)(period * L);
+  cur_slot = slot_of(0, 0);
+  issue(cur, cur_slot);
   for (int step = 0; step < L; ++step) {
     if constexpr (RK4) {
       // classical RK4 (proposed.cpp:141-168) as in the resident kernel, with
       // the K-sum folded into the Q plane: X0 = Q, X1 = X2/X4, X2 = X3
-      const double h = p.h;
+      const double h = wh;
       double *Qr = X0r, *Qi = X0i, *Yr = X1r, *Yi = X1i, *Zr = X2r, *Zi = X2i;
       FOR_OWN {
         if (!live(m)) continue;
@@ -929,19 +963,19 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
       // splitting (proposed.cpp:170-194), as in the resident kernel
       int r0 = 0;
       if (fsal && step > 0) {
-        drift_swap(odrift[0]);
+        drift_swap(wdrift(0));
         r0 = 1;
       }
       for (int r = r0; r < nocc; ++r) {
         const bool last = (r == nocc - 1);
         const int nstep = last ? step + 1 : step;
         const int nr = last ? (fsal ? 1 : 0) : r + 1;
-        if (p.variant == 0) drift_swap(odrift[r]);
+        if (p.variant == 0) drift_swap(wdrift(r));
         double2* box = begin_occ(nstep, nr);
         slab_gemm<C>(acc, box, soff, raddr, Ar, Ai, warp, lane, kmax, n);
       CPROF(1);
         end_occ(nstep, nr);
-        const double kc = (fsal && last && step + 1 < L) ? p.fsal_kick : okick[r];
+        const double kc = (fsal && last && step + 1 < L) ? wfsal : wkick(r);
         FOR_OWN {
           if (!live(m)) continue;
           double q0[4];
@@ -950,9 +984,9 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
 #pragma unroll
           for (int q = 0; q < 4; ++q) P[m][nb][q] -= kc * (acc[m][nb][q] + g2 * q0[q]);
         }
-        if (p.variant == 1 && !last) drift_swap(odrift[r]);
+        if (p.variant == 1 && !last) drift_swap(wdrift(r));
       }
-      if (p.variant == 0) drift_swap(p.final_drift);
+      if (p.variant == 0) drift_swap(wfin);
     }
 
     // ---------------- end of step: finite check + Gershgorin over the cluster
@@ -1052,21 +1086,22 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
       }
       if (BD > 0.0) {
         code = 1;
-        fail_step = step;
+        fail_step = step_off + step;
         break;
       }
       const double xi = n == 0 ? 1.0 : (ND > 0.0 ? inf_d() : H / Lo);
       if (xi > p.threshold) {
         // P <- P Q^-1, Q <- I (proposed.cpp:196-202)
         cp_async_wait_all();  // the prefetched box of the next occurrence stays in its buffer
-        if (!isfinite(xi)) ++npiv;
+        const bool main = !(BULK && bulk_phase);  // SolveStats counts the slab solve only (proposed.cpp:328)
+        if (main && !isfinite(xi)) ++npiv;
         CPROF(4);
         write_slabs(false);
         const bool ok = cluster_solve();
         CPROF(3);
         if (!ok) {
           code = 2;
-          fail_step = step;
+          fail_step = step_off + step;
           break;
         }
         // X rows -> M1 (own rows; only this CTA read them), then slab columns -> P
@@ -1105,7 +1140,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
           set_q_diag(Ar, Ai, false);
         }
         __syncthreads();
-        ++rhst;
+        if (main) ++rhst;
         CPROF(5);
       }
       CPROF(4);
@@ -1113,30 +1148,137 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
   }
   cp_async_wait_all();
   __syncthreads();
+  if (code) break;
 
   CPROF(2);
-  // ---------------- surface solve: X = R T^-1 (proposed.cpp:204-208), rho = X[:, 0]
-  if (code == 0) {
-    write_slabs(true);
-    const bool ok = cluster_solve();
-    if (!ok) {
-      code = 3;
-      fail_step = L;
-    } else {
-      const double s0 = p.sin_theta0[pair];
-      const double g0 = p.gdiag[pair * n].x;
-      for (int lr = tid; lr < SW; lr += CNT) {
-        const int i = col0 + lr;
-        if (i >= n) continue;
-        const int o = sw<NP>(lr, 0);
-        const double2 rho = make_double2(Br_[o], Bi_[o]);
-        const double2 gi = p.gdiag[pair * n + i];
-        const bool prop = gi.y == 0.0;  // geometry.cpp:46-50
-        p.rho[pair * n + i] = rho;
-        p.eta[pair * n + i] = prop ? (rho.x * rho.x + rho.y * rho.y) * s0 * g0 / gi.x : 0.0;
-      }
+  // ---------------- surface solve: X = R T^-1 (proposed.cpp:204-208), rho = X[:, 0].
+  // In the bulk phase the full X is the period's R and the state continues.
+  if (BULK && bulk_phase) {  // the solve overwrites the Q planes: keep the own slab
+    FOR_OWN {
+      double q0[4];
+      ld(Ar, Ai, m, nb, q0);
+      const long o = (long)orow(m) * NP + col0 + ocol(nb);
+      *reinterpret_cast<double2*>(M3r + o) = make_double2(q0[0], q0[1]);
+      *reinterpret_cast<double2*>(M3i + o) = make_double2(q0[2], q0[3]);
     }
   }
+  write_slabs(true);
+  const bool ok = cluster_solve();
+  if (!ok) {
+    code = (BULK && bulk_phase) ? 4 : 3;  // "bulk reflection read: ..." / "reflection extraction: ..."
+    fail_step = (BULK && bulk_phase) ? (int)period : L;
+    break;
+  }
+  if (!(BULK && bulk_phase)) {
+    const double s0 = p.sin_theta0[pair];
+    const double g0 = p.gdiag[pair * n].x;
+    for (int lr = tid; lr < SW; lr += CNT) {
+      const int i = col0 + lr;
+      if (i >= n) continue;
+      const int o = sw<NP>(lr, 0);
+      const double2 rho = make_double2(Br_[o], Bi_[o]);
+      const double2 gi = p.gdiag[pair * n + i];
+      const bool prop = gi.y == 0.0;  // geometry.cpp:46-50
+      p.rho[pair * n + i] = rho;
+      p.eta[pair * n + i] = prop ? (rho.x * rho.x + rho.y * rho.y) * s0 * g0 / gi.x : 0.0;
+    }
+    break;
+  }
+  if constexpr (BULK) {
+    // ---- ||R - R_prev||_F <= tol max(1, ||R||_F) (proposed.cpp:334-339) over
+    // the own rows of R, reduced over the cluster in rank order
+    double dn = 0.0, rn = 0.0;
+    for (int w = tid; w < SW * (NP / 2); w += CNT) {
+      const int lr2 = w / (NP / 2), j = 2 * (w % (NP / 2));
+      const int i2 = col0 + lr2;
+      if (i2 >= n) continue;
+      const int so = sw<NP>(lr2, j);
+      double2 xr = *reinterpret_cast<const double2*>(Br_ + so);
+      double2 xi = *reinterpret_cast<const double2*>(Bi_ + so);
+      if (j >= n) xr.x = xi.x = 0.0;
+      if (j + 1 >= n) xr.y = xi.y = 0.0;
+      const long o = (long)i2 * NP + j;
+      if (period > 0) {
+        const double2 pr = *reinterpret_cast<const double2*>(Rr + o);
+        const double2 pi = *reinterpret_cast<const double2*>(Ri + o);
+        const double d0 = xr.x - pr.x, d1 = xr.y - pr.y, d2 = xi.x - pi.x, d3 = xi.y - pi.y;
+        dn += d0 * d0 + d1 * d1 + d2 * d2 + d3 * d3;
+      }
+      rn += xr.x * xr.x + xr.y * xr.y + xi.x * xi.x + xi.y * xi.y;
+      *reinterpret_cast<double2*>(Rr + o) = xr;
+      *reinterpret_cast<double2*>(Ri + o) = xi;
+    }
+    dn = warp_sum(dn);
+    rn = warp_sum(rn);
+    if (lane == 0) {
+      sc->red_a[warp] = dn;
+      sc->red_b[warp] = rn;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double a = 0.0, b = 0.0;
+      for (int w = 0; w < CNW; ++w) {
+        a += sc->red_a[w];
+        b += sc->red_b[w];
+      }
+      pubv[5] = a;
+      pubv[6] = b;
+    }
+    cl.sync();  // partial norms and every CTA's R rows visible
+    double D = 0.0, Rn = 0.0;
+    for (int r = 0; r < cs; ++r) {
+      const double* rv = cl.map_shared_rank(pubv, r);
+      D += rv[5];
+      Rn += rv[6];
+    }
+    cl.sync();  // pubv free again
+    if (!(period > 0 && sqrt(D) <= p.bulk_tol * fmax(1.0, sqrt(Rn)))) {
+      if (++period >= p.bulk_max_periods) {
+        code = 5;  // ConvergenceError: the bulk R did not settle
+        fail_step = (int)period;
+        break;
+      }
+      FOR_OWN {  // the next period continues from the saved state
+        const long o = (long)orow(m) * NP + col0 + ocol(nb);
+        const double2 a = *reinterpret_cast<const double2*>(M3r + o);
+        const double2 b = *reinterpret_cast<const double2*>(M3i + o);
+        const double q0[4] = {a.x, a.y, b.x, b.y};
+        st(Ar, Ai, m, nb, q0);
+      }
+      __syncthreads();
+      again = true;
+      continue;
+    }
+    // ---- seeded slab: Q = G^-1 (I + R) / 2, P = (i/2)(I - R) (proposed.cpp:114-128)
+    FOR_OWN {
+      const int r = orow(m);
+      const double2 gv = r < n ? p.ginv[pair * n + r] : make_double2(0.0, 0.0);
+      const long o = (long)r * NP + col0 + ocol(nb);
+      double2 rr = make_double2(0.0, 0.0), ri = rr;
+      if (r < n) {
+        rr = *reinterpret_cast<const double2*>(Rr + o);
+        ri = *reinterpret_cast<const double2*>(Ri + o);
+      }
+      double q0[4];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = col0 + ocol(nb) + e;
+        const double dlt = (r == c && r < n) ? 1.0 : 0.0;
+        const double re = (e ? rr.y : rr.x), im = (e ? ri.y : ri.x);
+        const double ar = 0.5 * (dlt + re), ai = 0.5 * im;  // (I + R) / 2
+        q0[e] = gv.x * ar - gv.y * ai;
+        q0[2 + e] = gv.x * ai + gv.y * ar;
+        P[m][nb][e] = 0.5 * im;  // (i/2)(I - R) = Im(R)/2 + i (1 - Re R)/2
+        P[m][nb][2 + e] = 0.5 * (dlt - re);
+      }
+      st(Ar, Ai, m, nb, q0);
+    }
+    __syncthreads();
+    bulk_phase = false;
+    period = 0;
+    again = true;
+  }
+  } while (BULK && again);
   CPROF(6);
 #ifdef MB_PROFILE
   if (tid == 0 && p.prof)
@@ -1157,7 +1299,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
 template <class C, bool RK4>
 cudaError_t launch_cfg(const PropagateParams& p, cudaStream_t st, int cs) {
   const Layout LY = cluster_layout(C::NP, C::SW, RK4 ? 3 : 2, p.box_size, p.ndiff);
-  auto kern = cluster_kernel<C, RK4>;
+  auto kern = p.bulk_steps > 0 ? cluster_kernel<C, RK4, true> : cluster_kernel<C, RK4, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LY.total);
   if (e != cudaSuccess) return e;
   if (cs > 8) {

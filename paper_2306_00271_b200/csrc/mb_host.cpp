@@ -504,8 +504,8 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
   int npad = mbx::propagate_supported(n, stepper->algorithm == MB_STEP_RK4);
   if (opts->path == 1 && !npad) fail(MB_ERR_CONFIG, "resident kernel does not cover this rod count / stepper");
   if (opts->path == 2 || opts->path == 3) npad = 0;
-  if (fields[0].has_bulk_period && !npad)
-    fail(MB_ERR_CONFIG, "bulk seeding runs in the resident kernel only (N <= 64, path 0 or 1)");
+  if (fields[0].has_bulk_period && opts->path == 2)
+    fail(MB_ERR_CONFIG, "bulk seeding runs in the resident and cluster kernels only (path 0, 1 or 3)");
   bool big = npad == 0;
   if (big) npad = (n + 7) & ~7;
 
@@ -611,7 +611,9 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
   // round 1): cluster wins for the 61-pair N=199 case, the batched path for
   // 4096 pairs at N=127/255.
   bool cluster = false;
-  if (big && (opts->path == 3 || (opts->path == 0 && npairs < 512))) {
+  // bulk seeding (per-pair period loop until R settles) exists only in the
+  // on-chip kernels, so it takes the cluster kernel at any batch size
+  if (big && (opts->path == 3 || (opts->path == 0 && (npairs < 512 || bulk)))) {
     const int rk4 = stepper->algorithm == MB_STEP_RK4;
     const size_t need = mbx::cluster_smem_bytes(n, rk4, box_size, ndiff);
     int optin = 0;
@@ -624,6 +626,11 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
       fail(MB_ERR_CONFIG, "cluster kernel does not cover this rod count / stepper / box size");
     }
   }
+
+  if (bulk && big)
+    fail(MB_ERR_CONFIG,
+         "bulk seeding runs in the resident (N <= 64) and cluster (64 < N <= 256) kernels only; "
+         "this rod count / stepper does not fit the cluster kernel's shared memory");
 
   mb_plan* pl = new mb_plan();
   pl->ctx = ctx;
@@ -783,7 +790,8 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
     pl->big = big;
     pl->cluster = cluster;
     pl->stride = (int)stride;
-    if (cluster) p.scratch = dev_alloc<double>(pl, (std::size_t)npairs * 6 * npad * npad);
+    // cluster kernel: A, B, panel rows (+ the saved Q slab of a bulk period)
+    if (cluster) p.scratch = dev_alloc<double>(pl, (std::size_t)npairs * (bulk ? 8 : 6) * npad * npad);
     if (big) {
       mbx::BigParams& b = pl->bp;
       b.n = n;

@@ -70,8 +70,8 @@ struct PropagateParams {
   double2* rho;               // [npairs][n]
   PointStatus* status;        // [npairs]
   unsigned long long* prof;   // [8] phase cycles (MB_PROFILE builds), may be null
-  double* scratch;            // cluster kernel: per pair 6 NP^2 doubles (RHST / surface solve)
-  // bulk seeding (proposed.cpp:311-342), resident kernel only; bulk_steps = 0: none
+  double* scratch;            // cluster kernel: per pair 6 NP^2 doubles (8 with a bulk period)
+  // bulk seeding (proposed.cpp:311-342), resident and cluster kernels; bulk_steps = 0: none
   int bulk_steps;             // steps per bulk period
   long bulk_base;             // first table slot of the bulk window
   double bulk_h, bulk_final_drift, bulk_fsal_kick;

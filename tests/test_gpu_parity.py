@@ -309,8 +309,14 @@ def test_bulk_atoms_parity(oracle, method):
     assert H.entry_rel_err(eta, ref) <= TOL
 
 
-def test_bulk_rejected_off_resident():
-    w = configs.config4(127, "sp6", n_structures=1).subset(theta0=[1.0], slices=10, z_bottom=-0.16)
+def test_bulk_rejected_off_chip():
+    """Bulk seeding lives in the on-chip kernels; rk4 at N > 128 does not fit
+    the cluster kernel and the batched path (path 2) has no period loop."""
+    w = configs.config4(255, "rk4", n_structures=1).subset(theta0=[1.0], slices=10, z_bottom=-0.16)
     w.bulk_period = 0.1
     with pytest.raises(mb.ConfigError):
         H.run_device(w)
+    w = configs.config4(127, "sp6", n_structures=1).subset(theta0=[1.0], slices=10, z_bottom=-0.16)
+    w.bulk_period = 0.1
+    with pytest.raises(mb.ConfigError):
+        H.run_device(w, path=2)

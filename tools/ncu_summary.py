@@ -35,7 +35,7 @@ KEYS = {
     "dram_throughput_pct": ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", 1),
 }
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1, "msecond": 1,
-        "nsecond": 1e-6}
+        "nsecond": 1e-6, "s": 1e3, "second": 1e3}
 
 
 def summarize(rep):
