@@ -150,7 +150,9 @@ typedef struct {
                             (same node height; exact in exact arithmetic). 0 = reference op order */
   int path;              /* 0 auto, 1 on-chip resident kernel (N <= 64),
                             2 batched large-N kernels (state in HBM, N <= 256),
-                            3 cluster-resident kernel (64 < N <= 256, one CTA cluster per pair) */
+                            3 cluster-resident kernel (64 < N <= 256, one CTA cluster per pair),
+                            4 the same kernel as persistent cooperative CTA groups exchanging
+                              through L2 (64 < N <= 256; auto picks 3 or 4 by co-residency) */
 } mb_options;
 
 /* one (structure, glancing angle) point */

@@ -429,7 +429,8 @@ class SweepOptions:
     residual_check: bool = True
     fsal: bool = False
     stepper: Optional[StepperSpec] = None  # custom splitting coefficients
-    path: int = 0              # 0 auto, 1 resident on-chip kernel, 2 batched large-N kernels
+    path: int = 0              # 0 auto, 1 resident on-chip kernel, 2 batched large-N kernels,
+    #                            3 cluster kernel, 4 cluster kernel as cooperative groups
 
     def _stepper(self):
         return self.stepper if self.stepper is not None else StepperSpec.by_name(self.method)

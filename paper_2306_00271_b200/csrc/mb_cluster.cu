@@ -1,1333 +1,14 @@
-// K2c: cluster-resident propagation for 64 < N <= 256 (SURVEY.md §8a row K2,
-// BASELINE north_star: "one thread-block cluster using DSMEM once the
-// complex128 matrices outgrow a single SM's shared memory").
-//
-// One cluster of CS = ceil(N/16) CTAs per (structure, angle) pair. CTA c owns
-// the 16-column slab [16c, 16c+16) of Q (shared memory) and P (registers) for
-// the whole slab: a kick P[:, slab] -= h b (U + G^2) Q[:, slab] and a drift
-// Q[:, slab] += h a P[:, slab] only touch the own slab, so the propagation runs
-// without any inter-CTA traffic. U is gathered from the node's coefficient box
-// (staged per CTA with cp.async, double-buffered) exactly as in the resident
-// kernel; the product runs as 3M DMMA tiles (mb_tiles.cuh).
-//
-// Cross-slab steps (all cluster-uniform decisions):
-//  * end-of-step check (proposed.cpp:279-287, kernels.cpp:82-99): finite check
-//    and Gershgorin row sums per slab, exchanged through DSMEM (two cluster
-//    barriers; every CTA reduces in the same order, so all take the same RHST
-//    decision);
-//  * RHST P <- P Q^-1 (proposed.cpp:196-202) and the surface solve
-//    X = R T^-1 (proposed.cpp:204-208): the slabs are written to a per-pair L2
-//    scratch, every CTA reads back a 16-ROW slab of [A; B], and the
-//    Gauss-Jordan column elimination with partial pivoting (Eigen's
-//    PartialPivLU of A^T, kernels.cpp:66-71) runs row-distributed: the owner of
-//    row k+1 updates it first and publishes the next pivot (column, 1/pivot,
-//    multiplier row) in its shared memory; every CTA reads it through DSMEM;
-//    one cluster barrier per pivot. Then the 1e-10 residual gate of
-//    solve_right (kernels.cpp:73-79) as DMMA tiles against the saved A in L2.
-#include <cooperative_groups.h>
-#include <cuda_runtime.h>
-
-#include <cstdint>
-
-#include "mb_device.cuh"
-#include "mb_internal.h"
-#include "mb_tiles.cuh"
-
-namespace cg = cooperative_groups;
-
-// MB_PROFILE builds: per-phase cycles of thread 0 of every CTA (slots as in
-// mb_kernels.cu: 0 table wait, 1 GEMM, 2 epilogue, 3 RHST solve, 4 check,
-// 5 RHST rest, 6 surface, 7 prologue)
-#ifdef MB_PROFILE
-#define CPROF(slot)                                 \
-  do {                                              \
-    const long long _t = clock64();                 \
-    prof_acc[slot] += _t - prof_t;                  \
-    prof_t = _t;                                    \
-  } while (0)
-#else
-#define CPROF(slot) \
-  do {              \
-  } while (0)
-#endif
+// K2c host side: variant choice (cluster vs cooperative groups), shared-memory
+// sizing and launch of the cluster-resident propagation kernel (mb_cluster.cuh).
+#include "mb_cluster.cuh"
 
 namespace mbx {
 
-namespace {
-
-constexpr int CNT = 256, CNW = 8;
-constexpr int WCH = 32;  // columns per DSMEM chunk of the blocked solve
-
-// SW = slab columns per CTA = rows per CTA in the solve layout (16 at NP=256,
-// 32 at NP=128: the wider slab gives the warps C64's 16x32 tile)
-template <int NP_, int SW_>
-struct CCfg {
-  static constexpr int NP = NP_, SW = SW_;
-  static constexpr int MB = NP / 64;  // row blocks per warp, interleaved: rb = warp + 8 m
-  static constexpr int NB = SW / 8;   // the slab's 8-column blocks
-  static constexpr int NQ = NP / 32;  // row entries per lane in the solve layout
-  static constexpr int MINB = 1;      // resident CTAs per SM
-  static constexpr int TPR = CNT / SW;      // threads per row in the row-layout phases
-  static constexpr int SLOTS = 2 * SW / TPR;  // special-column slots per thread
-};
-
-// slab plane [NP rows][SW cols]. SW=16: the XOR puts rows r and r+1 in
-// opposite bank halves; SW=32: rows r..r+3 rotate by 4 doubles. Both keep the
-// B fragments (4 rows x 8 cols) and own-element double2 accesses conflict-free.
-template <int SW>
-__device__ __forceinline__ int ss(int r, int c) {
-  if constexpr (SW == 16)
-    return r * 16 + (c ^ ((r & 1) << 3));
-  else
-    return r * SW + (c ^ ((r & 3) << 2));
-}
-
-struct Layout {
-  size_t planes, boxes, fpub, tpub, tloc, wch, scr, g2s, rsum, dsum, pubv, occ, soff, sboxpos, total;
-};
-
-__host__ __device__ inline size_t al16(size_t b) { return (b + 15) & ~(size_t)15; }
-
-__host__ __device__ inline Layout cluster_layout(int np, int SW, int nq, int box_size, int ndiff) {
-  Layout L{};
-  size_t o = 0;
-  L.planes = o;
-  o += al16((size_t)nq * 2 * np * SW * sizeof(double));
-  L.boxes = o;
-  o += al16((size_t)2 * box_size * sizeof(double2));
-  L.fpub = o;
-  o += al16((size_t)2 * np * sizeof(double2));
-  L.tpub = o;  // published panel table: 1/pivot, |pivot|^2, pivot column, flag
-  o += al16((size_t)(3 * SW + 1) * sizeof(double2));
-  L.tloc = o;  // special columns, pivot slots, mask; F on special columns; 1/pivots, |pivot|^2
-  o += al16((size_t)(8 * SW + 2 * SW * SW + 2 * SW) * sizeof(double2));
-  L.wch = o;  // W chunk: 16 panel rows x WCH columns, re/im
-  o += al16((size_t)2 * SW * WCH * sizeof(double));
-  L.scr = o;
-  o += al16(sizeof(Scratch));
-  L.g2s = o;
-  o += al16((size_t)np * sizeof(double));
-  L.rsum = o;
-  o += al16((size_t)np * sizeof(double));
-  L.dsum = o;
-  o += al16((size_t)np * sizeof(double));
-  L.pubv = o;
-  o += al16(8 * sizeof(double));
-  L.occ = o;  // occ_kick, occ_drift, bulk kick, bulk drift (double) then occ_node (int), kMaxOcc each
-  o += al16((size_t)kMaxOcc * (4 * sizeof(double) + sizeof(int)));
-  L.soff = o;
-  o += al16((size_t)np * sizeof(int));
-  L.sboxpos = o;
-  o += al16((size_t)ndiff * sizeof(int));
-  L.total = o;
-  return L;
-}
-
-// 3M box GEMM on the slab: acc = U[rows of the warp's blocks, :] * X[:, slab]
-template <class C>
-__device__ __forceinline__ void slab_gemm(double (&acc)[C::MB][C::NB][4], const double2* __restrict__ box,
-                                          const int* __restrict__ soff, const int (&raddr)[C::MB],
-                                          const double* __restrict__ Xr, const double* __restrict__ Xi, int warp,
-                                          int lane, int kmax, int n) {
-  const int kl = lane & 3, cl = lane >> 2;
-  double t1[C::MB][C::NB][2], t2[C::MB][C::NB][2], t3[C::MB][C::NB][2];
-#pragma unroll
-  for (int m = 0; m < C::MB; ++m)
-#pragma unroll
-    for (int nb = 0; nb < C::NB; ++nb)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) t1[m][nb][e] = t2[m][nb][e] = t3[m][nb][e] = 0.0;
-#pragma unroll 2
-  for (int k0 = 0; k0 < kmax; k0 += 4) {
-    const int k = k0 + kl;
-    const int offk = soff[k];
-    double br[C::NB], bi[C::NB], bs[C::NB];
-#pragma unroll
-    for (int nb = 0; nb < C::NB; ++nb) {
-      const int o = ss<C::SW>(k, nb * 8 + cl);
-      br[nb] = Xr[o];
-      bi[nb] = Xi[o];
-      bs[nb] = br[nb] + bi[nb];
-    }
-#pragma unroll
-    for (int m = 0; m < C::MB; ++m) {
-      if (8 * (warp + 8 * m) >= n) continue;  // warp-uniform: block of padding rows
-      double2 a = make_double2(0.0, 0.0);
-      if (raddr[m] >= 0) a = box[raddr[m] - offk];
-      const double as = a.x + a.y;
-#pragma unroll
-      for (int nb = 0; nb < C::NB; ++nb) dmma(t1[m][nb][0], t1[m][nb][1], a.x, br[nb]);
-#pragma unroll
-      for (int nb = 0; nb < C::NB; ++nb) dmma(t2[m][nb][0], t2[m][nb][1], a.y, bi[nb]);
-#pragma unroll
-      for (int nb = 0; nb < C::NB; ++nb) dmma(t3[m][nb][0], t3[m][nb][1], as, bs[nb]);
-    }
-  }
-#pragma unroll
-  for (int m = 0; m < C::MB; ++m)
-#pragma unroll
-    for (int nb = 0; nb < C::NB; ++nb)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        acc[m][nb][e] = t1[m][nb][e] - t2[m][nb][e];
-        acc[m][nb][2 + e] = (t3[m][nb][e] - t1[m][nb][e]) - t2[m][nb][e];
-      }
-}
-
-// residual tile configuration (SW rows x NP/8 columns per warp)
-template <int NP_, int SW_>
-struct RCfg {
-  static constexpr int NP = NP_, MB = SW_ / 8, NB = NP / 64;
-};
-
-// BULK: the bulk-layer seed (compute_bulk_reflection_proposed,
-// proposed.cpp:311-342) runs first, as in the resident kernel; compiled
-// separately so the plain kernels keep their registers.
-template <class C, bool RK4, bool BULK>
-__global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_constant__ PropagateParams p) {
-  constexpr int NP = C::NP, MB = C::MB, NB = C::NB, NQ = C::NQ, SW = C::SW, TPR = C::TPR, SLOTS = C::SLOTS;
-  constexpr int PL = NP * SW;  // doubles per slab plane
-  cg::cluster_group cl = cg::this_cluster();
-  const int cs = (int)cl.num_blocks();
-  const int crank = (int)cl.block_rank();
-  const long pair = blockIdx.x / cs;
-  const int col0 = SW * crank;  // global column of slab column 0 (= first own row in the solve layout)
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int n = p.n;
-#ifdef MB_PROFILE
-  long long prof_t = clock64(), prof_acc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-#endif
-
-  extern __shared__ __align__(16) unsigned char smem[];
-  const Layout LY = cluster_layout(NP, SW, RK4 ? 3 : 2, p.box_size, p.ndiff);
-  double* const planes = reinterpret_cast<double*>(smem + LY.planes);
-  double2* const boxes = reinterpret_cast<double2*>(smem + LY.boxes);
-  double2* const fpub = reinterpret_cast<double2*>(smem + LY.fpub);  // [2][NP] panel multiplier rows
-  double2* const tpub = reinterpret_cast<double2*>(smem + LY.tpub);  // panel table
-  double2* const tloc = reinterpret_cast<double2*>(smem + LY.tloc);  // consumer tables
-  double* const wchr = reinterpret_cast<double*>(smem + LY.wch);     // [16][WCH]
-  double* const wchi = wchr + SW * WCH;
-  Scratch* const sc = reinterpret_cast<Scratch*>(smem + LY.scr);
-  double* const g2s = reinterpret_cast<double*>(smem + LY.g2s);
-  double* const rsum = reinterpret_cast<double*>(smem + LY.rsum);
-  double* const dsum = reinterpret_cast<double*>(smem + LY.dsum);
-  double* const pubv = reinterpret_cast<double*>(smem + LY.pubv);  // [0..3] check, [4] bad, [5..7] residual
-  double* const okick = reinterpret_cast<double*>(smem + LY.occ);  // runtime-indexed
-  double* const odrift = okick + kMaxOcc;                            // stepper tables in
-  double* const bkick = odrift + kMaxOcc;                            // shared memory
-  double* const bdrift = bkick + kMaxOcc;                            // (bulk window: h_bulk)
-  int* const onode = reinterpret_cast<int*>(bdrift + kMaxOcc);
-  int* const soff = reinterpret_cast<int*>(smem + LY.soff);
-  int* const sboxpos = reinterpret_cast<int*>(smem + LY.sboxpos);
-  // slab planes: X0, X1 (, X2) re/im
-  double* const X0r = planes;
-  double* const X0i = planes + PL;
-  double* const X1r = planes + 2 * PL;
-  double* const X1i = planes + 3 * PL;
-  double* const X2r = planes + 4 * PL;
-  double* const X2i = planes + 5 * PL;
-  // solve layout (aliases X0, X1): own rows of A and B, [16][NP] swizzled
-  double* const Ar_ = planes;
-  double* const Ai_ = planes + SW * NP;
-  double* const Br_ = planes + 2 * SW * NP;
-  double* const Bi_ = planes + 3 * SW * NP;
-  // per-pair L2 scratch: M0 (A), M1 (B), row-major NP x NP planes
-  const long NN = (long)NP * NP;
-  double* const M0r = p.scratch + pair * (BULK ? 8 : 6) * NN;
-  double* const M0i = M0r + NN;
-  double* const M1r = M0r + 2 * NN;
-  double* const M1i = M0r + 3 * NN;
-  // M2: the panel rows of A after factorisation (multiplier rows F), written
-  // by each panel's owner and read by every CTA from L2. DSMEM is the wrong
-  // channel for this broadcast: the owner's shared-memory port would serve
-  // all CS-1 readers (~20 B/clk per SM, producer pays).
-  double* const M2r = M0r + 4 * NN;
-  double* const M2i = M0r + 5 * NN;
-
-  // M3: the own Q slab saved across a bulk period's reflection read
-  double* const M3r = M0r + 6 * NN;
-  double* const M3i = M0r + 7 * NN;
-  const double2* coef = p.coef + (long)p.pair_struct[pair] * p.nslots * p.ndiff;
-  const int kmax = (n + 3) & ~3;
-  for (int i = tid; i < p.ndiff; i += CNT) sboxpos[i] = p.boxpos[i];
-  if (tid == 0) *reinterpret_cast<volatile int*>(tpub + 3 * SW) = 0;  // panel flag
-  for (int i = tid; i < kMaxOcc; i += CNT) {
-    okick[i] = p.occ_kick[i];
-    odrift[i] = p.occ_drift[i];
-    bkick[i] = BULK ? p.bulk_kick[i] : 0.0;
-    bdrift[i] = BULK ? p.bulk_drift[i] : 0.0;
-    onode[i] = p.occ_node[i];
-  }
-  // box holes are read for the padded k in [n, kmax) (times zero rows of X):
-  // keep them zero, never stale shared memory
-  for (int i = tid; i < 2 * p.box_size; i += CNT) boxes[i] = make_double2(0.0, 0.0);
-  for (int i = tid; i < NP; i += CNT) {
-    soff[i] = i < n ? p.rowoff[i] : 0;
-    g2s[i] = i < n ? p.gamma2[pair * n + i] : 0.0;
-  }
-
-  // own elements: block m -> rows 8 (warp + 8 m) + lane/4, block nb -> slab
-  // columns 8 nb + 2 (lane & 3) + {0, 1}
-  auto orow = [&](int m) { return 8 * (warp + 8 * m) + (lane >> 2); };
-  auto ocol = [&](int nb) { return 8 * nb + 2 * (lane & 3); };
-  auto live = [&](int m) { return 8 * (warp + 8 * m) < n; };
-  auto ld = [&](const double* Xr, const double* Xi, int m, int nb, double (&v)[4]) {
-    const int o = ss<SW>(orow(m), ocol(nb));
-    const double2 a = *reinterpret_cast<const double2*>(Xr + o);
-    const double2 b = *reinterpret_cast<const double2*>(Xi + o);
-    v[0] = a.x;
-    v[1] = a.y;
-    v[2] = b.x;
-    v[3] = b.y;
-  };
-  auto st = [&](double* Xr, double* Xi, int m, int nb, const double (&v)[4]) {
-    const int o = ss<SW>(orow(m), ocol(nb));
-    *reinterpret_cast<double2*>(Xr + o) = make_double2(v[0], v[1]);
-    *reinterpret_cast<double2*>(Xi + o) = make_double2(v[2], v[3]);
-  };
-#define FOR_OWN _Pragma("unroll") for (int m = 0; m < MB; ++m) _Pragma("unroll") for (int nb = 0; nb < NB; ++nb)
-
-  // current / next Q planes
-  double* Ar = X0r;
-  double* Ai = X0i;
-  double* Nr = X1r;
-  double* Ni = X1i;
-  // initial_state (proposed.cpp:123-128): Q = diag(ginv)/2, P = (i/2) I
-  auto set_q_diag = [&](double* Xr, double* Xi, bool ginv_half) {
-    for (int w = tid; w < PL; w += CNT) {
-      Xr[w] = 0.0;
-      Xi[w] = 0.0;
-    }
-    __syncthreads();
-    for (int c = tid; c < SW; c += CNT) {
-      const int i = col0 + c;
-      if (i < n) {
-        const double2 g = ginv_half ? p.ginv[pair * n + i] : make_double2(2.0, 0.0);
-        Xr[ss<SW>(i, c)] = 0.5 * g.x;
-        Xi[ss<SW>(i, c)] = 0.5 * g.y;
-      }
-    }
-  };
-  set_q_diag(Ar, Ai, true);
-  double P[MB][NB][4];
-  FOR_OWN {
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int r = orow(m), c = col0 + ocol(nb) + e;
-      P[m][nb][e] = 0.0;
-      P[m][nb][2 + e] = (r == c && r < n) ? 0.5 : 0.0;
-    }
-  }
-  int raddr[MB];
-#pragma unroll
-  for (int m = 0; m < MB; ++m) {
-    const int r = orow(m);
-    raddr[m] = r < n ? p.box_center + p.rowoff[r] : -1;
-  }
-  double acc[MB][NB][4];
-
-  // the propagation window: the slab (main) or one bulk period (bulk seeding,
-  // proposed.cpp:311-321: the same stepper on the bulk window's step)
-  bool bulk_phase = BULK && p.bulk_steps > 0;
-  auto wbase = [&]() -> long { return (BULK && bulk_phase) ? p.bulk_base : 0L; };
-  auto wkick = [&](int r) -> double { return (BULK && bulk_phase) ? bkick[r] : okick[r]; };
-  auto wdrift = [&](int r) -> double { return (BULK && bulk_phase) ? bdrift[r] : odrift[r]; };
-  auto slot_of = [&](int step, int r) -> long { return wbase() + (long)step * p.slot_stride + onode[r]; };
-  auto issue = [&](double2* dst, long slot) {
-    const double2* src = coef + slot * p.ndiff;
-    for (int d = tid; d < p.ndiff; d += CNT) cp_async16(dst + sboxpos[d], src + d);
-    cp_async_commit();
-  };
-  double2* cur = boxes;
-  double2* nxt = boxes + p.box_size;
-  __syncthreads();
-  CPROF(7);
-  long cur_slot = 0;
-
-  int rhst = 0, npiv = 0, code = 0, fail_step = 0;
-  const int nocc = p.nocc;
-  int L = p.nsteps;
-  const bool fsal = !RK4 && p.fsal && p.variant == 1;
-
-  auto begin_occ = [&](int nstep, int nr) -> double2* {
-    CPROF(2);
-    cp_async_wait_all();
-    __syncthreads();
-    CPROF(0);
-    if (nstep < L) {
-      const long ns = slot_of(nstep, nr);
-      if (ns != cur_slot) issue(nxt, ns);
-    }
-    return cur;
-  };
-  auto end_occ = [&](int nstep, int nr) {
-    if (nstep < L) {
-      const long ns = slot_of(nstep, nr);
-      if (ns != cur_slot) {
-        double2* t = cur;
-        cur = nxt;
-        nxt = t;
-        cur_slot = ns;
-      }
-    }
-  };
-  auto drift_swap = [&](double c) {
-    FOR_OWN {  // every block, padding rows included: they must stay exactly zero
-      double q0[4];
-      ld(Ar, Ai, m, nb, q0);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) q0[q] += c * P[m][nb][q];
-      st(Nr, Ni, m, nb, q0);
-    }
-    double* t = Ar;
-    Ar = Nr;
-    Nr = t;
-    t = Ai;
-    Ai = Ni;
-    Ni = t;
-  };
-
-  // ---------------------------------------------------------------- solve
-  // B <- B A^-1 for the matrices the caller wrote to (M0, M1); returns the
-  // cluster-uniform success flag. Own rows of the solution end in Br_/Bi_.
-  // Blocked Gauss-Jordan column elimination with partial pivoting, row
-  // distributed (Eigen's PartialPivLU of A^T, kernels.cpp:66-71; same pivot
-  // sequence as the unblocked elimination). Panel b = the 16 own rows of CTA
-  // b. (1) CTA b factorises its panel locally: for k in the panel, pivot p_k =
-  // first argmax_{j>=k} |A[k][j]| on row k, op k applied to its later panel
-  // rows; row k (after ops < k) stays in place and defines the multipliers
-  // F_k[j] = A[k][j] (j != k, p_k; F_k[p_k] = A[k][k], F_k[k] = 0, 0 for j >= n).
-  // (2) every CTA applies the 16 ops to its rows (A rows of later panels, all
-  // B rows): first on the <= 32 "special" columns {k} u {p_k} that the swaps
-  // touch (sequentially, giving x_k(i) = X[i][p_k] / A[k][p_k]), then on all
-  // other columns as one rank-16 update X[:, j] -= sum_k x_k F_k[j] with F
-  // read from the owner's rows through DSMEM in column chunks. One cluster
-  // barrier per panel; the next owner factorises right after its own update.
-  // panel factorisation on the owner (chain as in gauss_jordan of the
-  // resident kernel: warp 0 updates row k+1 and computes its pivot while the
-  // other warps update the remaining panel rows; one CTA barrier per step).
-  // Publishes the pivot table and raises the CTA's panel flag to `sid`.
-  auto factor_panel = [&](int sid) {
-    const int kend = min(n, col0 + SW), nk = kend - col0;
-    int* ptp = reinterpret_cast<int*>(tpub + 2 * SW);     // [16] pivot columns
-    double2* ptinv = tpub;                                // [16] 1/pivot
-    double* ptpv = reinterpret_cast<double*>(tpub + SW);  // [16] |pivot|^2
-    if (warp == 0 && nk > 0) {
-      double2 a[NQ];
-#pragma unroll
-      for (int q = 0; q < NQ; ++q) {
-        const int j = lane + 32 * q;
-        a[q] = make_double2(Ar_[sw<NP>(0, j)], Ai_[sw<NP>(0, j)]);
-      }
-      gj_pivot<C>(a, col0, n, fpub, *sc, 0, lane);
-    }
-    __syncthreads();
-    for (int lk = 0; lk < nk; ++lk) {
-      const int k = col0 + lk, slot = lk & 1;
-      const int piv = sc->piv[slot];
-      const double2 inv = sc->inv[slot];
-      if (tid == 32) {
-        ptp[lk] = piv;
-        ptinv[lk] = inv;
-        ptpv[lk] = sc->pivval[slot];
-      }
-      double2 fj[NQ];
-#pragma unroll
-      for (int q = 0; q < NQ; ++q) fj[q] = fpub[slot * NP + lane + 32 * q];
-      if (warp == 0 && lk + 1 < nk) {  // chain: row k+1, then its pivot
-        const int rows[1] = {lk + 1};
-        const bool isA[1] = {true};
-        double2 row[1][NQ];
-        gj_rows<C, 1>(Ar_, Ai_, Br_, Bi_, rows, isA, k, piv, inv, fj, row, lane);
-        gj_pivot<C>(row[0], k + 1, n, fpub + (slot ^ 1) * NP, *sc, slot ^ 1, lane);
-      }
-      for (int lr = lk + 2 + (warp - 1); warp > 0 && lr < nk; lr += CNW - 1) {
-        const int rows[1] = {lr};
-        const bool isA[1] = {true};
-        double2 row[1][NQ];
-        gj_rows<C, 1>(Ar_, Ai_, Br_, Bi_, rows, isA, k, piv, inv, fj, row, lane);
-      }
-      __syncthreads();
-    }
-    // publish the panel rows (F) to L2 for the consumers
-    for (int w = tid; w < nk * (NP / 2); w += CNT) {
-      const int lr = w / (NP / 2), j = 2 * (w % (NP / 2));
-      const int so = sw<NP>(lr, j);
-      const long o = (long)(col0 + lr) * NP + j;
-      *reinterpret_cast<double2*>(M2r + o) = *reinterpret_cast<const double2*>(Ar_ + so);
-      *reinterpret_cast<double2*>(M2i + o) = *reinterpret_cast<const double2*>(Ai_ + so);
-    }
-    __syncthreads();
-    if (tid == 0) {
-      __threadfence();  // tables and rows visible cluster-wide before the flag
-      *reinterpret_cast<volatile int*>(tpub + 3 * SW) = sid;
-    }
-  };
-  auto wait_panel = [&](int b, int sid) {
-    if (tid == 0) {
-      unsigned a = (unsigned)__cvta_generic_to_shared(tpub + 3 * SW), ra;
-      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(b));
-      int v;
-      do {
-        asm volatile("ld.acquire.cluster.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(ra) : "memory");
-      } while (v != sid);
-    }
-    __syncthreads();
-  };
-
-  int solve_id = 0;
-  auto solve_blocked = [&]() -> bool {
-    const int npan = (n + SW - 1) / SW;
-    const int sid = ++solve_id;
-    CPROF(11);
-    if (crank == 0) factor_panel(sid);
-    CPROF(8);
-    int* scol = reinterpret_cast<int*>(tloc);                   // [32] special columns
-    int* pslot = scol + 2 * SW;                                 // [16] slot of p_k
-    unsigned* smask = reinterpret_cast<unsigned*>(pslot + SW);  // [NP/32] special-column bitmask
-    int* sn = reinterpret_cast<int*>(smask + NP / 32);          // [1] special count
-    int* lpp = sn + 1;                                          // [16] pivot columns
-    double2* fs = tloc + 8 * SW;                                // [16][32] F on special columns
-    double2* linv = fs + 2 * SW * SW;                           // [16] 1/pivot
-    double* lpv = reinterpret_cast<double*>(linv + SW);         // [16] |pivot|^2
-    // TPR threads per row: lr = tid / TPR (SW rows), slots cg + TPR u
-    const int lr = tid / TPR, cg = tid % TPR, gi = col0 + lr;
-    const int rbase = lane & ~(TPR - 1);
-    bool okb = true;
-    for (int b = 0; b < npan; ++b) {
-      wait_panel(b, sid);
-      CPROF(9);
-      const int p0 = b * SW, nk = min(SW, n - p0);
-      const double2* rt = cl.map_shared_rank(tpub, b);
-      const double* war = M2r + (long)p0 * NP;  // panel rows, row-major, ld NP
-      const double* wai = M2i + (long)p0 * NP;
-      if (tid < SW) {
-        linv[tid] = rt[tid];
-        lpp[tid] = reinterpret_cast<const int*>(rt + 2 * SW)[tid];
-        lpv[tid] = reinterpret_cast<const double*>(rt + SW)[tid];
-      }
-      __syncthreads();
-      // special columns: the panel's, then pivots outside it (first occurrence,
-      // in pivot order), built by one warp (lane lk <-> pivot lk; SW <= 32)
-      if (warp == 0) {
-        const unsigned FULL = 0xffffffffu, lower = (1u << lane) - 1u;
-        const bool has = lane < nk;
-        const int pk = has ? lpp[lane] : -1;
-        const bool bad = has && !(lpv[lane] > 0.0);
-        const bool inpan = has && pk >= p0 && pk < p0 + SW;
-        const bool outside = has && !inpan;
-        const unsigned outm = __ballot_sync(FULL, outside);
-        const unsigned same = __match_any_sync(FULL, outside ? pk : -1 - lane) & outm;
-        const bool first = outside && (same & lower) == 0u;
-        const unsigned firstm = __ballot_sync(FULL, first);
-        const int cnt = SW + __popc(firstm);
-        if (inpan) pslot[lane] = pk - p0;
-        if (outside) pslot[lane] = SW + __popc(firstm & ((1u << (__ffs(same) - 1)) - 1u));
-        for (int q = lane; q < NP / 32; q += 32) smask[q] = 0u;
-        if (lane < SW) scol[lane] = p0 + lane;
-        if (first) scol[SW + __popc(firstm & lower)] = pk;
-        for (int c = cnt + lane; c < 2 * SW; c += 32) scol[c] = -1;
-        __syncwarp();
-        if (lane < SW && p0 + lane < NP) atomicOr(&smask[(p0 + lane) >> 5], 1u << ((p0 + lane) & 31));
-        if (first) atomicOr(&smask[pk >> 5], 1u << (pk & 31));
-        const bool anybad = __any_sync(FULL, bad);
-        if (lane == 0) sn[0] = anybad ? -1 : cnt;
-      }
-      __syncthreads();
-      if (sn[0] < 0) {  // zero pivot: the same owner data everywhere
-        okb = false;
-        break;
-      }
-      // F restricted to special columns: fs[lk][s]
-      for (int w = tid; w < SW * 2 * SW; w += CNT) {
-        const int lk = w / (2 * SW), sl = w % (2 * SW);
-        const int j = scol[sl];
-        double2 f = make_double2(0.0, 0.0);
-        if (lk < nk && j >= 0 && j < n) {
-          const int k = p0 + lk, pk = lpp[lk];
-          const int jj = (j == pk) ? k : j;  // F_k[p_k] = A[k][k]
-          if (j != k) f = make_double2(__ldcg(war + (long)lk * NP + jj), __ldcg(wai + (long)lk * NP + jj));
-        }
-        fs[w] = f;
-      }
-      __syncthreads();
-      CPROF(10);
-      // apply the panel's 16 ops to the own A rows (half 0) or B rows (half 1)
-      auto consume = [&](int half) {
-        const bool isA = half == 0;
-        if (isA && col0 + SW <= p0 + SW) return;  // CTA-uniform: no A rows below the panel
-        double* Xr = isA ? Ar_ : Br_;
-        double* Xi = isA ? Ai_ : Bi_;
-        const bool act = gi < n && (isA ? gi >= p0 + SW : true);
-        // (A) sequential ops on the special columns
-        double2 val[SLOTS];
-#pragma unroll
-        for (int u = 0; u < SLOTS; ++u) {
-          const int j = scol[cg + TPR * u];
-          val[u] = (act && j >= 0) ? make_double2(Xr[sw<NP>(lr, j)], Xi[sw<NP>(lr, j)]) : make_double2(0.0, 0.0);
-        }
-        double2 xk[SW];
-#pragma unroll
-        for (int lk = 0; lk < SW; ++lk) {
-          xk[lk] = make_double2(0.0, 0.0);
-          if (lk < nk) {
-            const int ps = pslot[lk], ks = lk;
-            auto pick = [&](int sl) {
-              double2 v = val[0];
-#pragma unroll
-              for (int u = 1; u < SLOTS; ++u)
-                if (sl / TPR == u) v = val[u];
-              return make_double2(__shfl_sync(0xffffffffu, v.x, rbase | (sl % TPR)),
-                                  __shfl_sync(0xffffffffu, v.y, rbase | (sl % TPR)));
-            };
-            const double2 xp = pick(ps);
-            const double2 xold = pick(ks);
-            const double2 x = cmul(xp, linv[lk]);
-            xk[lk] = x;
-#pragma unroll
-            for (int u = 0; u < SLOTS; ++u) {
-              const int sl = cg + TPR * u;
-              const double2 f = fs[lk * 2 * SW + sl];
-              const double2 v = (sl == ps) ? xold : val[u];
-              const double2 nv = make_double2(v.x - (f.x * x.x - f.y * x.y), v.y - (f.x * x.y + f.y * x.x));
-              val[u] = (sl == ks) ? x : nv;
-            }
-          }
-        }
-        if (act) {
-#pragma unroll
-          for (int u = 0; u < SLOTS; ++u) {
-            const int j = scol[cg + TPR * u];
-            if (j >= 0) {
-              Xr[sw<NP>(lr, j)] = val[u].x;
-              Xi[sw<NP>(lr, j)] = val[u].y;
-            }
-          }
-        }
-        // (B) other columns: X[i][j] -= sum_k x_k F_k[j] (F_k[j] = A[k][j]),
-        // F chunks from the owner through DSMEM, next chunk prefetched into
-        // registers while the current one is applied
-        // SW x WCH chunk, FR double2 per thread and plane
-        constexpr int FR = SW * (WCH / 2) / CNT;
-        auto fetch = [&](int j0, double2 (&a)[FR], double2 (&c)[FR]) {
-#pragma unroll
-          for (int f = 0; f < FR; ++f) {
-            const int w = tid + f * CNT, ldt = w / (WCH / 2), j = j0 + 2 * (w % (WCH / 2));
-            a[f] = make_double2(0.0, 0.0);
-            c[f] = a[f];
-            if (ldt < nk && j < NP) {
-              const long o = (long)ldt * NP + j;
-              a[f] = __ldcg(reinterpret_cast<const double2*>(war + o));
-              c[f] = __ldcg(reinterpret_cast<const double2*>(wai + o));
-            }
-            if (j >= n || ((smask[j >> 5] >> (j & 31)) & 1u)) a[f].x = c[f].x = 0.0;
-            if (j + 1 >= n || ((smask[(j + 1) >> 5] >> ((j + 1) & 31)) & 1u)) a[f].y = c[f].y = 0.0;
-          }
-        };
-        double2 na[FR], nc[FR];
-        fetch(0, na, nc);
-        for (int j0 = 0; j0 < n; j0 += WCH) {
-          __syncthreads();  // previous chunk consumed (and the special write-back done)
-#pragma unroll
-          for (int f = 0; f < FR; ++f) {
-            const int w = tid + f * CNT, ldt = w / (WCH / 2), ldj = 2 * (w % (WCH / 2));
-            *reinterpret_cast<double2*>(wchr + ldt * WCH + ldj) = na[f];
-            *reinterpret_cast<double2*>(wchi + ldt * WCH + ldj) = nc[f];
-          }
-          __syncthreads();
-          if (j0 + WCH < n) fetch(j0 + WCH, na, nc);
-          if (act) {
-#pragma unroll
-            for (int u = 0; u < WCH / TPR; ++u) {
-              const int jj = cg + TPR * u, j = j0 + jj;
-              if (j >= n) continue;
-              const int o = sw<NP>(lr, j);
-              double xr = Xr[o], xi = Xi[o];
-#pragma unroll
-              for (int t = 0; t < SW; ++t) {
-                const double wr = wchr[t * WCH + jj], wi = wchi[t * WCH + jj];
-                xr -= xk[t].x * wr - xk[t].y * wi;
-                xi -= xk[t].x * wi + xk[t].y * wr;
-              }
-              Xr[o] = xr;
-              Xi[o] = xi;
-            }
-          }
-        }
-        __syncthreads();
-      };
-      consume(0);  // A rows first: the next owner's panel depends on them
-      CPROF(11);
-      if (crank == b + 1) factor_panel(sid);
-      CPROF(8);
-      consume(1);
-      CPROF(11);
-    }
-    // an owner's rows and table are immutable for the rest of the solve, so
-    // consumers may lag; one barrier before any of them is reused
-    cl.sync();
-    CPROF(9);
-    return okb;
-  };
-
-  auto cluster_solve = [&]() -> bool {
-    CPROF(5);
-    cl.sync();  // M0 / M1 slabs of every CTA are visible
-    CPROF(8);
-    // own 16 rows of A and B (rows >= n and columns >= n are zero)
-    for (int w = tid; w < SW * (NP / 2); w += CNT) {
-      const int lr = w / (NP / 2), j = 2 * (w % (NP / 2));
-      const int i = col0 + lr;
-      double2 ar = make_double2(0.0, 0.0), ai = ar, br = ar, bi = ar;
-      if (i < n && j < n) {  // columns >= 16 cs are never written: mask to n
-        const long o = (long)i * NP + j;
-        ar = *reinterpret_cast<const double2*>(M0r + o);
-        ai = *reinterpret_cast<const double2*>(M0i + o);
-        br = *reinterpret_cast<const double2*>(M1r + o);
-        bi = *reinterpret_cast<const double2*>(M1i + o);
-        if (j + 1 >= n) ar.y = ai.y = br.y = bi.y = 0.0;
-      }
-      const int so = sw<NP>(lr, j);
-      *reinterpret_cast<double2*>(Ar_ + so) = ar;
-      *reinterpret_cast<double2*>(Ai_ + so) = ai;
-      *reinterpret_cast<double2*>(Br_ + so) = br;
-      *reinterpret_cast<double2*>(Bi_ + so) = bi;
-    }
-    __syncthreads();
-    CPROF(9);
-    const bool ok = solve_blocked();
-    if (!ok) return false;
-    if (!p.residual_check) return true;
-    CPROF(11);
-    // residual gate ||X A0 - B0||_F <= 1e-10 ||B0||_F over the cluster
-    // (kernels.cpp:73-79): own 16 rows of X times A0 (L2), k-chunks of 16 rows
-    // staged into the (now free) A rows area
-    using R = RCfg<NP, SW>;
-    double racc[R::MB][R::NB][4];
-#pragma unroll
-    for (int a = 0; a < R::MB; ++a)
-#pragma unroll
-      for (int b = 0; b < R::NB; ++b)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) racc[a][b][q] = 0.0;
-    const int wc0 = warp * (NP / CNW);
-    for (int k0 = 0; k0 < kmax; k0 += 16) {
-      __syncthreads();
-      for (int w = tid; w < 16 * (NP / 2); w += CNT) {
-        const int kk = w / (NP / 2), j = 2 * (w % (NP / 2));
-        const int kr = k0 + kk;
-        double2 ar = make_double2(0.0, 0.0), ai = ar;
-        if (kr < n && j < n) {
-          const long o = (long)kr * NP + j;
-          ar = *reinterpret_cast<const double2*>(M0r + o);
-          ai = *reinterpret_cast<const double2*>(M0i + o);
-          if (j + 1 >= n) ar.y = ai.y = 0.0;
-        }
-        const int so = sw<NP>(kk, j);
-        *reinterpret_cast<double2*>(Ar_ + so) = ar;
-        *reinterpret_cast<double2*>(Ai_ + so) = ai;
-      }
-      __syncthreads();
-#pragma unroll
-      for (int kk = 0; kk < 16; kk += 4) {
-        const int kl = kk + (lane & 3);
-        double ar[R::MB], ai[R::MB], an[R::MB];
-#pragma unroll
-        for (int a = 0; a < R::MB; ++a) {
-          const int o = sw<NP>(8 * a + (lane >> 2), k0 + kl);
-          ar[a] = Br_[o];
-          ai[a] = Bi_[o];
-          an[a] = dneg(ai[a]);
-        }
-        double br[R::NB], bi[R::NB];
-#pragma unroll
-        for (int b = 0; b < R::NB; ++b) {
-          const int o = sw<NP>(kl, wc0 + 8 * b + (lane >> 2));
-          br[b] = Ar_[o];
-          bi[b] = Ai_[o];
-        }
-        cmma<R>(racc, ar, ai, an, br, bi);
-      }
-    }
-    double rn = 0.0, bn = 0.0, bad = 0.0;
-#pragma unroll
-    for (int a = 0; a < R::MB; ++a)
-#pragma unroll
-      for (int b = 0; b < R::NB; ++b)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int i = col0 + 8 * a + (lane >> 2), j = wc0 + 8 * b + 2 * (lane & 3) + e;
-          if (i < n && j < n) {
-            const long o = (long)i * NP + j;
-            const double tr = M1r[o], ti = M1i[o];
-            const double dr = racc[a][b][e] - tr, di = racc[a][b][2 + e] - ti;
-            rn += dr * dr + di * di;
-            bn += tr * tr + ti * ti;
-            if (!isfinite(racc[a][b][e]) || !isfinite(racc[a][b][2 + e])) bad = 1.0;
-          }
-        }
-    rn = warp_sum(rn);
-    bn = warp_sum(bn);
-    bad = warp_sum(bad);
-    if (lane == 0) {
-      sc->red_a[warp] = rn;
-      sc->red_b[warp] = bn;
-      sc->red_i[warp] = bad > 0.0;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      double a = 0.0, b = 0.0, f = 0.0;
-      for (int w = 0; w < CNW; ++w) {
-        a += sc->red_a[w];
-        b += sc->red_b[w];
-        f += sc->red_i[w];
-      }
-      pubv[5] = a;
-      pubv[6] = b;
-      pubv[7] = f;
-    }
-    cl.sync();
-    double Rn = 0.0, Bn = 0.0, F = 0.0;
-    for (int r = 0; r < cs; ++r) {
-      const double* rv = cl.map_shared_rank(pubv, r);
-      Rn += rv[5];
-      Bn += rv[6];
-      F += rv[7];
-    }
-    cl.sync();  // pubv[5..7] free again
-    CPROF(10);
-    const double bnorm = sqrt(Bn);
-    return sqrt(Rn) / (bnorm > 0.0 ? bnorm : 1.0) <= 1e-10 && F == 0.0;
-  };
-
-  // write own slab elements of A (from the Q plane) and B (P registers) to M0/M1
-  auto write_slabs = [&](bool surface) {
-    FOR_OWN {
-      const int r = orow(m);
-      if (r >= n) continue;
-      const double2 g = surface ? p.gdiag[pair * n + r] : make_double2(0.0, 0.0);
-      double q0[4];
-      ld(Ar, Ai, m, nb, q0);
-      double a[4], b[4];
-      if (surface) {  // T = G Q - i P, R = G Q + i P
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const double qr = q0[e], qi = q0[2 + e];
-          const double gqr = g.x * qr - g.y * qi, gqi = g.x * qi + g.y * qr;
-          const double pr = P[m][nb][e], pi = P[m][nb][2 + e];
-          a[e] = gqr + pi;
-          a[2 + e] = gqi - pr;
-          b[e] = gqr - pi;
-          b[2 + e] = gqi + pr;
-        }
-      } else {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          a[q] = q0[q];
-          b[q] = P[m][nb][q];
-        }
-      }
-      const long o = (long)r * NP + col0 + ocol(nb);
-      *reinterpret_cast<double2*>(M0r + o) = make_double2(a[0], a[1]);
-      *reinterpret_cast<double2*>(M0i + o) = make_double2(a[2], a[3]);
-      *reinterpret_cast<double2*>(M1r + o) = make_double2(b[0], b[1]);
-      *reinterpret_cast<double2*>(M1i + o) = make_double2(b[2], b[3]);
-    }
-  };
-
-  // Windows (run_window, proposed.cpp:275-289): with a bulk period, one bulk
-  // period after another (compute_bulk_reflection_proposed, proposed.cpp:
-  // 311-342) until R settles, then the slab from the seeded state; each window
-  // ends with extract_reflection (proposed.cpp:204-208).
-  long period = 0;
-  double* const Rr = BULK ? p.bulk_scratch + pair * 2 * NN : nullptr;  // previous R (row-major)
-  double* const Ri = BULK ? Rr + NN : nullptr;
-  bool again = false;  // BULK: another window follows
-  do {
-  again = false;
-  L = (BULK && bulk_phase) ? p.bulk_steps : p.nsteps;
-  const double wh = (BULK && bulk_phase) ? p.bulk_h : p.h;
-  const double wfin = (BULK && bulk_phase) ? p.bulk_final_drift : p.final_drift;
-  const double wfsal = (BULK && bulk_phase) ? p.bulk_fsal_kick : p.fsal_kick;
-  const int step_off = (int)(period * L);
-  cur_slot = slot_of(0, 0);
-  issue(cur, cur_slot);
-  for (int step = 0; step < L; ++step) {
-    if constexpr (RK4) {
-      // classical RK4 (proposed.cpp:141-168) as in the resident kernel, with
-      // the K-sum folded into the Q plane: X0 = Q, X1 = X2/X4, X2 = X3
-      const double h = wh;
-      double *Qr = X0r, *Qi = X0i, *Yr = X1r, *Yi = X1i, *Zr = X2r, *Zi = X2i;
-      FOR_OWN {
-        if (!live(m)) continue;
-        double v[4];
-        ld(Qr, Qi, m, nb, v);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) v[q] += (0.5 * h) * P[m][nb][q];
-        st(Yr, Yi, m, nb, v);
-      }
-      double2* box = begin_occ(step, 1);
-      slab_gemm<C>(acc, box, soff, raddr, Qr, Qi, warp, lane, kmax, n);
-      CPROF(1);
-      end_occ(step, 1);
-      FOR_OWN {
-        if (!live(m)) continue;
-        double q0[4], x2[4];
-        ld(Qr, Qi, m, nb, q0);
-        ld(Yr, Yi, m, nb, x2);
-        const double g2 = g2s[orow(m)];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const double K = -(acc[m][nb][q] + g2 * q0[q]);
-          acc[m][nb][q] = K;
-          x2[q] += (0.25 * h * h) * K;
-        }
-        st(Zr, Zi, m, nb, x2);
-      }
-      __syncthreads();  // every warp finished reading Q in the stage-1 GEMM
-      FOR_OWN {
-        if (!live(m)) continue;
-        double q0[4];
-        ld(Qr, Qi, m, nb, q0);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          q0[q] += h * P[m][nb][q];
-          P[m][nb][q] += (h / 6.0) * acc[m][nb][q];
-        }
-        st(Qr, Qi, m, nb, q0);
-      }
-      box = begin_occ(step, 2);
-      slab_gemm<C>(acc, box, soff, raddr, Yr, Yi, warp, lane, kmax, n);
-      CPROF(1);
-      end_occ(step, 2);
-      FOR_OWN {
-        if (!live(m)) continue;
-        double x2[4];
-        ld(Yr, Yi, m, nb, x2);
-        const double g2 = g2s[orow(m)];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const double K = -(acc[m][nb][q] + g2 * x2[q]);
-          acc[m][nb][q] = K;
-          P[m][nb][q] += (h / 3.0) * K;
-        }
-      }
-      __syncthreads();
-      FOR_OWN {
-        if (!live(m)) continue;
-        double qb[4], x2[4], x3[4], x4[4];
-        ld(Qr, Qi, m, nb, qb);
-        ld(Yr, Yi, m, nb, x2);
-        ld(Zr, Zi, m, nb, x3);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          x4[q] = qb[q] + (0.5 * h * h) * acc[m][nb][q];
-          qb[q] += (h * h / 6.0) * acc[m][nb][q] + (2.0 / 3.0) * (x3[q] - x2[q]);
-        }
-        st(Yr, Yi, m, nb, x4);
-        st(Qr, Qi, m, nb, qb);
-      }
-      box = begin_occ(step, 3);
-      slab_gemm<C>(acc, box, soff, raddr, Zr, Zi, warp, lane, kmax, n);
-      CPROF(1);
-      end_occ(step, 3);
-      FOR_OWN {
-        if (!live(m)) continue;
-        double x3[4], qb[4];
-        ld(Zr, Zi, m, nb, x3);
-        ld(Qr, Qi, m, nb, qb);
-        const double g2 = g2s[orow(m)];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const double K = -(acc[m][nb][q] + g2 * x3[q]);
-          qb[q] += (h * h / 6.0) * K;
-          P[m][nb][q] += (h / 3.0) * K;
-        }
-        st(Qr, Qi, m, nb, qb);
-      }
-      box = begin_occ(step + 1, 0);
-      slab_gemm<C>(acc, box, soff, raddr, Yr, Yi, warp, lane, kmax, n);
-      CPROF(1);
-      end_occ(step + 1, 0);
-      FOR_OWN {
-        if (!live(m)) continue;
-        double x4[4];
-        ld(Yr, Yi, m, nb, x4);
-        const double g2 = g2s[orow(m)];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) P[m][nb][q] += (h / 6.0) * -(acc[m][nb][q] + g2 * x4[q]);
-      }
-      Ar = Qr;
-      Ai = Qi;
-    } else {
-      // splitting (proposed.cpp:170-194), as in the resident kernel
-      int r0 = 0;
-      if (fsal && step > 0) {
-        drift_swap(wdrift(0));
-        r0 = 1;
-      }
-      for (int r = r0; r < nocc; ++r) {
-        const bool last = (r == nocc - 1);
-        const int nstep = last ? step + 1 : step;
-        const int nr = last ? (fsal ? 1 : 0) : r + 1;
-        if (p.variant == 0) drift_swap(wdrift(r));
-        double2* box = begin_occ(nstep, nr);
-        slab_gemm<C>(acc, box, soff, raddr, Ar, Ai, warp, lane, kmax, n);
-      CPROF(1);
-        end_occ(nstep, nr);
-        const double kc = (fsal && last && step + 1 < L) ? wfsal : wkick(r);
-        FOR_OWN {
-          if (!live(m)) continue;
-          double q0[4];
-          ld(Ar, Ai, m, nb, q0);
-          const double g2 = g2s[orow(m)];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) P[m][nb][q] -= kc * (acc[m][nb][q] + g2 * q0[q]);
-        }
-        if (p.variant == 1 && !last) drift_swap(wdrift(r));
-      }
-      if (p.variant == 0) drift_swap(wfin);
-    }
-
-    // ---------------- end of step: finite check + Gershgorin over the cluster
-    CPROF(2);
-    {
-      int bad = 0;
-      FOR_OWN {
-        double q0[4];
-        ld(Ar, Ai, m, nb, q0);
-        if (orow(m) >= n) q0[0] = q0[1] = q0[2] = q0[3] = 0.0;
-        double rs = 0.0, dg = 0.0;
-        const int r = orow(m);
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int c = col0 + ocol(nb) + e;
-          bad |= !isfinite(q0[e]) || !isfinite(q0[2 + e]) || !isfinite(P[m][nb][e]) ||
-                 !isfinite(P[m][nb][2 + e]);
-          const double a = sqrt(q0[e] * q0[e] + q0[2 + e] * q0[2 + e]);
-          if (c == r)
-            dg = a;
-          else if (c < n)
-            rs += a;
-        }
-        // nb blocks are folded by the caller loop order: accumulate in smem below
-        rs += __shfl_xor_sync(0xffffffffu, rs, 1);
-        rs += __shfl_xor_sync(0xffffffffu, rs, 2);
-        dg += __shfl_xor_sync(0xffffffffu, dg, 1);
-        dg += __shfl_xor_sync(0xffffffffu, dg, 2);
-        if ((lane & 3) == 0) {
-          if (nb == 0) {
-            rsum[r] = rs;
-            dsum[r] = dg;
-          } else {
-            rsum[r] += rs;
-            dsum[r] += dg;
-          }
-        }
-      }
-      bad = __syncthreads_or(bad);
-      if (tid == 0) pubv[4] = bad ? 1.0 : 0.0;
-      cl.sync();  // #1: slab partials visible
-      const int lr = tid / TPR, src = tid % TPR, i = col0 + lr;  // cs <= TPR
-      double Rr = 0.0, Dd = 0.0, Bf = 0.0;
-      if (src < cs) {
-        if (i < n) {
-          Rr = cl.map_shared_rank(rsum, src)[i];
-          Dd = cl.map_shared_rank(dsum, src)[i];
-        }
-        if (lr == 0) Bf = cl.map_shared_rank(pubv, src)[4];
-      }
-#pragma unroll
-      for (int o = TPR / 2; o > 0; o >>= 1) {
-        Rr += __shfl_xor_sync(0xffffffffu, Rr, o);
-        Dd += __shfl_xor_sync(0xffffffffu, Dd, o);
-        Bf = fmax(Bf, __shfl_xor_sync(0xffffffffu, Bf, o));
-      }
-      double hi = 0.0, lo = inf_d(), nd = 0.0;
-      if (i < n) {
-        hi = Dd + Rr;
-        lo = Dd - Rr;
-        nd = (Dd - Rr <= 0.0) ? 1.0 : 0.0;
-      }
-#pragma unroll
-      for (int o = TPR; o < 32; o <<= 1) {  // the warp's 32/TPR rows
-        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-        nd = fmax(nd, __shfl_xor_sync(0xffffffffu, nd, o));
-        Bf = fmax(Bf, __shfl_xor_sync(0xffffffffu, Bf, o));
-      }
-      if (lane == 0) {
-        sc->red_a[warp] = hi;
-        sc->red_b[warp] = lo;
-        sc->red_i[warp] = (nd > 0.0 ? 1 : 0) | (Bf > 0.0 ? 2 : 0);
-      }
-      __syncthreads();
-      if (tid == 0) {
-        double H = 0.0, Lo = inf_d();
-        int fl = 0;
-        for (int w = 0; w < CNW; ++w) {
-          H = fmax(H, sc->red_a[w]);
-          Lo = fmin(Lo, sc->red_b[w]);
-          fl |= sc->red_i[w];
-        }
-        pubv[0] = H;
-        pubv[1] = Lo;
-        pubv[2] = (fl & 1) ? 1.0 : 0.0;
-        pubv[3] = (fl & 2) ? 1.0 : 0.0;
-      }
-      cl.sync();  // #2: per-CTA row-block results visible
-      double H = 0.0, Lo = inf_d(), ND = 0.0, BD = 0.0;
-      for (int r = 0; r < cs; ++r) {
-        const double* rv = cl.map_shared_rank(pubv, r);
-        H = fmax(H, rv[0]);
-        Lo = fmin(Lo, rv[1]);
-        ND = fmax(ND, rv[2]);
-        BD = fmax(BD, rv[3]);
-      }
-      if (BD > 0.0) {
-        code = 1;
-        fail_step = step_off + step;
-        break;
-      }
-      const double xi = n == 0 ? 1.0 : (ND > 0.0 ? inf_d() : H / Lo);
-      if (xi > p.threshold) {
-        // P <- P Q^-1, Q <- I (proposed.cpp:196-202)
-        cp_async_wait_all();  // the prefetched box of the next occurrence stays in its buffer
-        const bool main = !(BULK && bulk_phase);  // SolveStats counts the slab solve only (proposed.cpp:328)
-        if (main && !isfinite(xi)) ++npiv;
-        CPROF(4);
-        write_slabs(false);
-        const bool ok = cluster_solve();
-        CPROF(3);
-        if (!ok) {
-          code = 2;
-          fail_step = step_off + step;
-          break;
-        }
-        // X rows -> M1 (own rows; only this CTA read them), then slab columns -> P
-        for (int w = tid; w < SW * (NP / 2); w += CNT) {
-          const int lr2 = w / (NP / 2), j = 2 * (w % (NP / 2));
-          const int i2 = col0 + lr2;
-          if (i2 < n) {
-            const int so = sw<NP>(lr2, j);
-            const long o = (long)i2 * NP + j;
-            *reinterpret_cast<double2*>(M1r + o) = *reinterpret_cast<const double2*>(Br_ + so);
-            *reinterpret_cast<double2*>(M1i + o) = *reinterpret_cast<const double2*>(Bi_ + so);
-          }
-        }
-        cl.sync();
-        FOR_OWN {
-          const int r = orow(m);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) P[m][nb][q] = 0.0;
-          if (r >= n) continue;
-          const long o = (long)r * NP + col0 + ocol(nb);
-          const double2 a = *reinterpret_cast<const double2*>(M1r + o);
-          const double2 b = *reinterpret_cast<const double2*>(M1i + o);
-          P[m][nb][0] = (col0 + ocol(nb) < n) ? a.x : 0.0;
-          P[m][nb][1] = (col0 + ocol(nb) + 1 < n) ? a.y : 0.0;
-          P[m][nb][2] = (col0 + ocol(nb) < n) ? b.x : 0.0;
-          P[m][nb][3] = (col0 + ocol(nb) + 1 < n) ? b.y : 0.0;
-        }
-        __syncthreads();
-        if constexpr (RK4) {
-          set_q_diag(X0r, X0i, false);
-          Ar = X0r;
-          Ai = X0i;
-          Nr = X1r;
-          Ni = X1i;
-        } else {
-          set_q_diag(Ar, Ai, false);
-        }
-        __syncthreads();
-        if (main) ++rhst;
-        CPROF(5);
-      }
-      CPROF(4);
-    }
-  }
-  cp_async_wait_all();
-  __syncthreads();
-  if (code) break;
-
-  CPROF(2);
-  // ---------------- surface solve: X = R T^-1 (proposed.cpp:204-208), rho = X[:, 0].
-  // In the bulk phase the full X is the period's R and the state continues.
-  if (BULK && bulk_phase) {  // the solve overwrites the Q planes: keep the own slab
-    FOR_OWN {
-      double q0[4];
-      ld(Ar, Ai, m, nb, q0);
-      const long o = (long)orow(m) * NP + col0 + ocol(nb);
-      *reinterpret_cast<double2*>(M3r + o) = make_double2(q0[0], q0[1]);
-      *reinterpret_cast<double2*>(M3i + o) = make_double2(q0[2], q0[3]);
-    }
-  }
-  write_slabs(true);
-  const bool ok = cluster_solve();
-  if (!ok) {
-    code = (BULK && bulk_phase) ? 4 : 3;  // "bulk reflection read: ..." / "reflection extraction: ..."
-    fail_step = (BULK && bulk_phase) ? (int)period : L;
-    break;
-  }
-  if (!(BULK && bulk_phase)) {
-    const double s0 = p.sin_theta0[pair];
-    const double g0 = p.gdiag[pair * n].x;
-    for (int lr = tid; lr < SW; lr += CNT) {
-      const int i = col0 + lr;
-      if (i >= n) continue;
-      const int o = sw<NP>(lr, 0);
-      const double2 rho = make_double2(Br_[o], Bi_[o]);
-      const double2 gi = p.gdiag[pair * n + i];
-      const bool prop = gi.y == 0.0;  // geometry.cpp:46-50
-      p.rho[pair * n + i] = rho;
-      p.eta[pair * n + i] = prop ? (rho.x * rho.x + rho.y * rho.y) * s0 * g0 / gi.x : 0.0;
-    }
-    break;
-  }
-  if constexpr (BULK) {
-    // ---- ||R - R_prev||_F <= tol max(1, ||R||_F) (proposed.cpp:334-339) over
-    // the own rows of R, reduced over the cluster in rank order
-    double dn = 0.0, rn = 0.0;
-    for (int w = tid; w < SW * (NP / 2); w += CNT) {
-      const int lr2 = w / (NP / 2), j = 2 * (w % (NP / 2));
-      const int i2 = col0 + lr2;
-      if (i2 >= n) continue;
-      const int so = sw<NP>(lr2, j);
-      double2 xr = *reinterpret_cast<const double2*>(Br_ + so);
-      double2 xi = *reinterpret_cast<const double2*>(Bi_ + so);
-      if (j >= n) xr.x = xi.x = 0.0;
-      if (j + 1 >= n) xr.y = xi.y = 0.0;
-      const long o = (long)i2 * NP + j;
-      if (period > 0) {
-        const double2 pr = *reinterpret_cast<const double2*>(Rr + o);
-        const double2 pi = *reinterpret_cast<const double2*>(Ri + o);
-        const double d0 = xr.x - pr.x, d1 = xr.y - pr.y, d2 = xi.x - pi.x, d3 = xi.y - pi.y;
-        dn += d0 * d0 + d1 * d1 + d2 * d2 + d3 * d3;
-      }
-      rn += xr.x * xr.x + xr.y * xr.y + xi.x * xi.x + xi.y * xi.y;
-      *reinterpret_cast<double2*>(Rr + o) = xr;
-      *reinterpret_cast<double2*>(Ri + o) = xi;
-    }
-    dn = warp_sum(dn);
-    rn = warp_sum(rn);
-    if (lane == 0) {
-      sc->red_a[warp] = dn;
-      sc->red_b[warp] = rn;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      double a = 0.0, b = 0.0;
-      for (int w = 0; w < CNW; ++w) {
-        a += sc->red_a[w];
-        b += sc->red_b[w];
-      }
-      pubv[5] = a;
-      pubv[6] = b;
-    }
-    cl.sync();  // partial norms and every CTA's R rows visible
-    double D = 0.0, Rn = 0.0;
-    for (int r = 0; r < cs; ++r) {
-      const double* rv = cl.map_shared_rank(pubv, r);
-      D += rv[5];
-      Rn += rv[6];
-    }
-    cl.sync();  // pubv free again
-    if (!(period > 0 && sqrt(D) <= p.bulk_tol * fmax(1.0, sqrt(Rn)))) {
-      if (++period >= p.bulk_max_periods) {
-        code = 5;  // ConvergenceError: the bulk R did not settle
-        fail_step = (int)period;
-        break;
-      }
-      FOR_OWN {  // the next period continues from the saved state
-        const long o = (long)orow(m) * NP + col0 + ocol(nb);
-        const double2 a = *reinterpret_cast<const double2*>(M3r + o);
-        const double2 b = *reinterpret_cast<const double2*>(M3i + o);
-        const double q0[4] = {a.x, a.y, b.x, b.y};
-        st(Ar, Ai, m, nb, q0);
-      }
-      __syncthreads();
-      again = true;
-      continue;
-    }
-    // ---- seeded slab: Q = G^-1 (I + R) / 2, P = (i/2)(I - R) (proposed.cpp:114-128)
-    FOR_OWN {
-      const int r = orow(m);
-      const double2 gv = r < n ? p.ginv[pair * n + r] : make_double2(0.0, 0.0);
-      const long o = (long)r * NP + col0 + ocol(nb);
-      double2 rr = make_double2(0.0, 0.0), ri = rr;
-      if (r < n) {
-        rr = *reinterpret_cast<const double2*>(Rr + o);
-        ri = *reinterpret_cast<const double2*>(Ri + o);
-      }
-      double q0[4];
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int c = col0 + ocol(nb) + e;
-        const double dlt = (r == c && r < n) ? 1.0 : 0.0;
-        const double re = (e ? rr.y : rr.x), im = (e ? ri.y : ri.x);
-        const double ar = 0.5 * (dlt + re), ai = 0.5 * im;  // (I + R) / 2
-        q0[e] = gv.x * ar - gv.y * ai;
-        q0[2 + e] = gv.x * ai + gv.y * ar;
-        P[m][nb][e] = 0.5 * im;  // (i/2)(I - R) = Im(R)/2 + i (1 - Re R)/2
-        P[m][nb][2 + e] = 0.5 * (dlt - re);
-      }
-      st(Ar, Ai, m, nb, q0);
-    }
-    __syncthreads();
-    bulk_phase = false;
-    period = 0;
-    again = true;
-  }
-  } while (BULK && again);
-  CPROF(6);
-#ifdef MB_PROFILE
-  if (tid == 0 && p.prof)
-    for (int q = 0; q < 12; ++q) atomicAdd(p.prof + q, (unsigned long long)prof_acc[q]);
-#endif
-  if (crank == 0 && tid == 0) {
-    PointStatus st;
-    st.code = code;
-    st.step = fail_step;
-    st.rhst = rhst;
-    st.reserved = npiv;  // RHSTs that needed the pivoting solve (non-dominant Q)
-    p.status[pair] = st;
-  }
-  cl.sync();  // no CTA leaves while a peer may still read its shared memory
-#undef FOR_OWN
-}
-
-template <class C, bool RK4>
-cudaError_t launch_cfg(const PropagateParams& p, cudaStream_t st, int cs) {
-  const Layout LY = cluster_layout(C::NP, C::SW, RK4 ? 3 : 2, p.box_size, p.ndiff);
-  auto kern = p.bulk_steps > 0 ? cluster_kernel<C, RK4, true> : cluster_kernel<C, RK4, false>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LY.total);
-  if (e != cudaSuccess) return e;
-  if (cs > 8) {
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (e != cudaSuccess) return e;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(p.npairs * cs));
-  cfg.blockDim = dim3(CNT);
-  cfg.dynamicSmemBytes = LY.total;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = (unsigned)cs;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, p);
-}
-
-}  // namespace
+cudaError_t cluster_dispatch_128(const PropagateParams& p, cudaStream_t st, int mode, int* groups_out);
+cudaError_t cluster_dispatch_256(const PropagateParams& p, cudaStream_t st, int mode, int* groups_out);
 
 // slab width per padded size: NP=256 -> 16 columns (CS <= 16); NP=128 -> 32
 // for splitting (CS <= 4), 16 for rk4 (its third slab plane does not fit at 32)
-#ifndef MB_SW128
-#define MB_SW128 32
-#endif
 static int cluster_sw(int np, int rk4) { return np == 128 && !rk4 ? MB_SW128 : 16; }
 
 size_t cluster_smem_bytes(int n, int rk4, int box_size, int ndiff) {
@@ -1338,16 +19,29 @@ size_t cluster_smem_bytes(int n, int rk4, int box_size, int ndiff) {
 
 int cluster_np(int n) { return n <= 64 || n > 256 ? 0 : (n <= 128 ? 128 : 256); }
 
+// mode 0: one thread-block cluster per pair; 1: cooperative groups.
+// groups_out != nullptr: only report how many groups run concurrently
+// (the instantiations live in mb_cluster_128.cu / mb_cluster_256.cu so they
+// compile in parallel)
+static cudaError_t dispatch(const PropagateParams& p, cudaStream_t st, int mode, int* groups_out) {
+  return p.n <= 128 ? cluster_dispatch_128(p, st, mode, groups_out) : cluster_dispatch_256(p, st, mode, groups_out);
+}
+
+int cluster_prefer_coop(const PropagateParams& p) {
+  int gcl = 0, gco = 0;
+  PropagateParams q = p;
+  q.coop_bar = nullptr;
+  if (dispatch(q, nullptr, 0, &gcl) != cudaSuccess) gcl = 0;
+  if (dispatch(q, nullptr, 1, &gco) != cudaSuccess) gco = 0;
+  cudaGetLastError();
+  if (gco <= 0) return 0;
+  if (gcl <= 0) return 1;
+  const long rcl = (p.npairs + gcl - 1) / gcl, rco = (p.npairs + gco - 1) / gco;
+  return rco < rcl ? 1 : 0;
+}
+
 cudaError_t launch_cluster(const PropagateParams& p, cudaStream_t st, int* launches) {
-  cudaError_t e;
-  if (p.n <= 128) {
-    constexpr int S = MB_SW128;
-    e = p.rk4 ? launch_cfg<CCfg<128, 16>, true>(p, st, (p.n + 15) / 16)
-              : launch_cfg<CCfg<128, S>, false>(p, st, (p.n + S - 1) / S);
-  } else {
-    const int cs = (p.n + 15) / 16;
-    e = p.rk4 ? launch_cfg<CCfg<256, 16>, true>(p, st, cs) : launch_cfg<CCfg<256, 16>, false>(p, st, cs);
-  }
+  const cudaError_t e = dispatch(p, st, p.coop ? 1 : 0, nullptr);
   if (e == cudaSuccess) ++*launches;
   return e == cudaSuccess ? cudaGetLastError() : e;
 }

@@ -503,9 +503,10 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
   if (n > 256) fail(MB_ERR_CONFIG, "device path supports at most 256 rods, got " + std::to_string(n));
   int npad = mbx::propagate_supported(n, stepper->algorithm == MB_STEP_RK4);
   if (opts->path == 1 && !npad) fail(MB_ERR_CONFIG, "resident kernel does not cover this rod count / stepper");
-  if (opts->path == 2 || opts->path == 3) npad = 0;
+  if (opts->path < 0 || opts->path > 4) fail(MB_ERR_ARG, "options: path must be 0..4");
+  if (opts->path >= 2) npad = 0;
   if (fields[0].has_bulk_period && opts->path == 2)
-    fail(MB_ERR_CONFIG, "bulk seeding runs in the resident and cluster kernels only (path 0, 1 or 3)");
+    fail(MB_ERR_CONFIG, "bulk seeding runs in the resident and cluster kernels only (path 0, 1, 3 or 4)");
   bool big = npad == 0;
   if (big) npad = (n + 7) & ~7;
 
@@ -613,7 +614,8 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
   bool cluster = false;
   // bulk seeding (per-pair period loop until R settles) exists only in the
   // on-chip kernels, so it takes the cluster kernel at any batch size
-  if (big && (opts->path == 3 || (opts->path == 0 && (npairs < 512 || bulk)))) {
+  const bool want_cluster = opts->path == 3 || opts->path == 4;
+  if (big && (want_cluster || (opts->path == 0 && (npairs < 512 || bulk)))) {
     const int rk4 = stepper->algorithm == MB_STEP_RK4;
     const size_t need = mbx::cluster_smem_bytes(n, rk4, box_size, ndiff);
     int optin = 0;
@@ -622,7 +624,7 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
     if (cluster) {
       big = false;
       npad = mbx::cluster_np(n);
-    } else if (opts->path == 3) {
+    } else if (want_cluster) {
       fail(MB_ERR_CONFIG, "cluster kernel does not cover this rod count / stepper / box size");
     }
   }
@@ -791,7 +793,19 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
     pl->cluster = cluster;
     pl->stride = (int)stride;
     // cluster kernel: A, B, panel rows (+ the saved Q slab of a bulk period)
-    if (cluster) p.scratch = dev_alloc<double>(pl, (std::size_t)npairs * (bulk ? 8 : 6) * npad * npad);
+    if (cluster) {
+      p.scratch = dev_alloc<double>(pl, (std::size_t)npairs * (bulk ? 8 : 6) * npad * npad);
+      // cluster or cooperative groups: path 3 / 4 force one; auto takes the
+      // variant that finishes the batch in fewer rounds of co-resident groups
+      p.coop = opts->path == 4 ? 1 : (opts->path == 3 ? 0 : mbx::cluster_prefer_coop(p));
+      if (p.coop) {
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+        const std::size_t maxc = (std::size_t)sms * mbx::kCoopMaxCtasPerSm;
+        p.coop_bar = dev_alloc<unsigned>(pl, maxc);
+        p.coop_pub = dev_alloc<double>(pl, maxc * mbx::kCoopPubDoubles);
+      }
+    }
     if (big) {
       mbx::BigParams& b = pl->bp;
       b.n = n;

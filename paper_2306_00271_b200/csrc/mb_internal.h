@@ -79,7 +79,17 @@ struct PropagateParams {
   long bulk_max_periods;
   double bulk_tol;
   double* bulk_scratch;       // per pair 2 NP^2 doubles: the previous period's R
+  // cluster kernel, cooperative variant (COOP): persistent groups of coop_cs
+  // co-resident CTAs exchanging through L2 instead of DSMEM
+  int coop;                   // 1: cooperative grid, 0: one thread-block cluster per pair
+  int coop_cs;                // CTAs per group (set by the launcher)
+  unsigned* coop_bar;         // [groups] barrier counters (zeroed by the launcher)
+  double* coop_pub;           // per CTA published arrays (kCoopPubDoubles each)
 };
+
+// upper bounds for the cooperative cluster variant's buffers
+constexpr int kCoopMaxCtasPerSm = 4;
+constexpr int kCoopPubDoubles = 2 * 256 + 8 + 2 * (3 * 32 + 1) + 2;
 
 // ---- large-N batched path (mb_large.cu): state in HBM, one launch per kick
 // or RK stage over all (pair, tile) work items, per-pair check and
@@ -139,6 +149,9 @@ int propagate_supported(int n, int rk4);  // padded size or 0
 // cluster-resident kernel (mb_cluster.cu) for 64 < n <= 256
 int cluster_np(int n);  // padded row count (128 / 256) or 0
 size_t cluster_smem_bytes(int n, int rk4, int box_size, int ndiff);
+// 1 when the cooperative variant finishes the batch in fewer rounds of
+// co-resident pair groups than thread-block clusters do (GPC packing)
+int cluster_prefer_coop(const PropagateParams& p);
 cudaError_t launch_cluster(const PropagateParams& p, cudaStream_t st, int* launches);
 
 }  // namespace mbx

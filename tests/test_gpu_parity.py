@@ -268,6 +268,25 @@ def test_cluster_matches_batched(n, method):
     assert H.curve_err(a, b) <= 1e-9
 
 
+@pytest.mark.parametrize("n,method", [(127, "sp6"), (199, "sp6"), (127, "rk4"), (81, "sp6")])
+def test_cooperative_groups_match_clusters(n, method):
+    """The cluster kernel as persistent cooperative CTA groups (path 4: L2
+    exchange, counter barriers, several pairs per group) computes exactly what
+    the thread-block clusters compute (path 3): same arithmetic, same
+    reduction orders. 26 pairs: more than one round of groups at every N.""" 
+    w = configs.config4(n, method, n_structures=2).subset(theta0=[0.5 + 0.45 * i for i in range(13)], slices=60,
+                                                         z_bottom=-0.96)
+    a, ra, sa = H.run_device(w, path=3)
+    b, rb, sb = H.run_device(w, path=4)
+    assert (sa["code"] == 0).all() and (sb["code"] == 0).all()
+    assert np.array_equal(sa["rhst"], sb["rhst"])
+    # two instantiations: the compiler may contract a few products into FMAs
+    # differently, so roundoff-level agreement, and each bitwise deterministic
+    assert H.curve_err(b, a) <= 1e-13
+    c, rc, sc = H.run_device(w, path=4)
+    assert np.array_equal(b, c) and np.array_equal(rb, rc)
+
+
 # ---------------------------------------------------------------- bulk seed (SURVEY §8f row 1)
 def test_bulk_fresnel_interface():  # test_proposed.cpp:281-298 through the device path
     """A constant potential continued periodically below z_bottom is a

@@ -19,6 +19,7 @@ ap.add_argument("--structures", type=int, default=0)
 ap.add_argument("--no-residual", action="store_true")
 ap.add_argument("--angles", type=int, default=0)
 ap.add_argument("--slices", type=int, default=0)
+ap.add_argument("--path", type=int, default=0)
 a = ap.parse_args()
 w = {0: configs.config0, 1: configs.config1, 3: configs.config3}.get(a.config, None)
 if w is not None:
@@ -31,7 +32,7 @@ if a.angles or a.slices:
     w = w.subset(theta0=list(w.theta0[:a.angles]) if a.angles else None, slices=a.slices or None)
 method = a.method or w.method
 rods = mb.RodSet.build_first(mb.Lattice2D(w.a1, w.a2), w.n_rods)
-opts = mb.SweepOptions(method=method, slices=w.slices, fsal=True, residual_check=not a.no_residual)
+opts = mb.SweepOptions(method=method, slices=w.slices, fsal=True, residual_check=not a.no_residual, path=a.path)
 pairs = [(s, t0, t1) for s in range(len(w.structures)) for t1 in w.theta1 for t0 in w.theta0]
 plan = mb.Plan(rods, configs.product_fields(w), w.gamma, pairs, opts)
 for _ in range(a.reps):
