@@ -22,12 +22,18 @@ struct Cfg {
   static_assert(TM % 8 == 0 && TN % 8 == 0, "tile must be a multiple of 8");
 };
 
-// swizzled row-major plane: element (r, c) of an NP x NP matrix. The XOR keeps
-// DMMA B-fragment loads (4 rows x 8 cols per warp) and dense A-fragment loads
-// (8 rows x 4 cols) free of bank conflicts without padding.
+// swizzled row-major plane: element (r, c) of an NP x NP matrix (NP >= 16).
+// Row r's columns are XORed with x_r = 0, 8, 4, 12 for r & 3 = 0..3:
+//  - DMMA B fragments (8-byte loads, 4 consecutive rows x 4 columns per
+//    16-lane phase) and dense A fragments (rows x 4 k) see four distinct
+//    column offsets mod 16, i.e. disjoint bank sets;
+//  - own-element double2 accesses (rows r, r+1 x 8 columns per 8-lane phase)
+//    see x_r and x_{r+1} differ in bit 3, so the two rows fill the low and
+//    high halves of the 128-byte bank window.
+// Both patterns are conflict-free without padding.
 template <int NP>
 __device__ __forceinline__ int sw(int r, int c) {
-  return r * NP + (c ^ ((r & 3) << 2));
+  return r * NP + (c ^ (((r & 1) << 3) | ((r & 2) << 1)));
 }
 
 // own-element accessors: v[mb][nb][0..3] = re(r,c), re(r,c+1), im(r,c), im(r,c+1)
