@@ -79,15 +79,12 @@ struct CCfg {
   static constexpr int SLOTS = 2 * SW / TPR;  // special-column slots per thread
 };
 
-// slab plane [NP rows][SW cols]. SW=16: the XOR puts rows r and r+1 in
-// opposite bank halves; SW=32: rows r..r+3 rotate by 4 doubles. Both keep the
-// B fragments (4 rows x 8 cols) and own-element double2 accesses conflict-free.
+// slab plane [NP rows][SW cols], the swizzle of sw<> (mb_tiles.cuh): x_r = 0,
+// 8, 4, 12 for r & 3 = 0..3 keeps the B fragments (4 rows x 4 columns per
+// phase) and the own-element double2 accesses (rows r, r+1) conflict-free.
 template <int SW>
 __device__ __forceinline__ int ss(int r, int c) {
-  if constexpr (SW == 16)
-    return r * 16 + (c ^ ((r & 1) << 3));
-  else
-    return r * SW + (c ^ ((r & 3) << 2));
+  return r * SW + (c ^ (((r & 1) << 3) | ((r & 2) << 1)));
 }
 
 struct Layout {

@@ -20,6 +20,7 @@ ap.add_argument("--no-residual", action="store_true")
 ap.add_argument("--angles", type=int, default=0)
 ap.add_argument("--slices", type=int, default=0)
 ap.add_argument("--path", type=int, default=0)
+ap.add_argument("--z-bottom", type=float, default=0.0)
 a = ap.parse_args()
 w = {0: configs.config0, 1: configs.config1, 3: configs.config3}.get(a.config, None)
 if w is not None:
@@ -28,8 +29,9 @@ elif a.config == 2:
     w = configs.config2(a.structures or 1024)
 else:
     w = configs.config4(a.n_rods, a.method or "rk4", n_structures=a.structures or 64)
-if a.angles or a.slices:
-    w = w.subset(theta0=list(w.theta0[:a.angles]) if a.angles else None, slices=a.slices or None)
+if a.angles or a.slices or a.z_bottom:
+    w = w.subset(theta0=list(w.theta0[:a.angles]) if a.angles else None, slices=a.slices or None,
+                 z_bottom=a.z_bottom or None)
 method = a.method or w.method
 rods = mb.RodSet.build_first(mb.Lattice2D(w.a1, w.a2), w.n_rods)
 opts = mb.SweepOptions(method=method, slices=w.slices, fsal=True, residual_check=not a.no_residual, path=a.path)
