@@ -422,26 +422,34 @@ __global__ void __launch_bounds__(NTH) big_check_kernel(const __grid_constant__ 
 // ------------------------------------------------------------------ Gauss-Jordan
 constexpr int GB = 16;  // panel rows
 
+// NPM: padded-size bound of the instantiation (128: 66 KB of panel state and
+// 2 CTAs per SM, so one CTA's pivot chain hides behind the other's updates;
+// 256: 130 KB, one CTA per SM)
+template <int NPM>
 struct GjSmem {
-  double rr[GB * NPMAX], ri[GB * NPMAX];  // panel rows of A (column ops applied)
-  double mr[GB * NPMAX], mi[GB * NPMAX];  // rows of E at the panel's pivot columns
+  double rr[GB * NPM], ri[GB * NPM];  // panel rows of A (column ops applied)
+  double mr[GB * NPM], mi[GB * NPM];  // rows of E at the panel's pivot columns
   double2 colp[2 * GB];
   double red_v[NTH / 32];
   int red_j[NTH / 32];
-  int pc[NPMAX];           // pivot column of row k
-  unsigned char used[NPMAX];
-  unsigned char inpanel[NPMAX];
+  int pc[NPM];           // pivot column of row k
+  unsigned char used[NPM];
+  unsigned char inpanel[NPM];
   int piv;
   double pivval;
   double sums[2][NTH / 32];
   int fail;
 };
-__device__ __forceinline__ int swg(int k, int c) { return k * NPMAX + (c ^ ((k & 3) << 2)); }
+template <int NPM>
+__device__ __forceinline__ int swg_(int k, int c) { return k * NPM + (c ^ ((k & 3) << 2)); }
 
 // 8x8 output tile c(rows r0.., cols c0..) += sum_k A(r, k) B(k, c) over k < K,
 // A and B read through functors returning complex values (double2)
 template <class FA, class FB>
 __device__ __forceinline__ void tile_gemm(double (&c)[4], int K, FA&& A, FB&& B, int lane) {
+  // the operands come from L2/HBM: unrolled so eight k-steps of loads are in
+  // flight before their DMMAs
+#pragma unroll 8
   for (int k0 = 0; k0 < K; k0 += 4) {
     const int k = k0 + (lane & 3);
     const double2 a = A(lane >> 2, k);
@@ -453,10 +461,12 @@ __device__ __forceinline__ void tile_gemm(double (&c)[4], int K, FA&& A, FB&& B,
   }
 }
 
-__global__ void __launch_bounds__(NTH, 1) big_gj_kernel(const __grid_constant__ BigParams p, int mode, int step,
+template <int NPM>
+__global__ void __launch_bounds__(NTH, NPM == 128 ? 2 : 1) big_gj_kernel(const __grid_constant__ BigParams p, int mode, int step,
                                                         int mq, int mp, int msa, int msb, int mx2, double h) {
   extern __shared__ __align__(16) unsigned char smem[];
-  GjSmem& g = *reinterpret_cast<GjSmem*>(smem);
+  GjSmem<NPM>& g = *reinterpret_cast<GjSmem<NPM>*>(smem);
+  auto swg = [](int k, int c) { return swg_<NPM>(k, c); };
   const long pair = blockIdx.x;
   if (p.status[pair].code != 0) return;
   if (mode == 0 && !(p.xi[pair] > p.threshold)) return;
@@ -475,11 +485,32 @@ __global__ void __launch_bounds__(NTH, 1) big_gj_kernel(const __grid_constant__ 
   if (mode == 0) {
     A = Qm;
     B = Pm;
-    if (p.residual_check)
-      for (long o = tid; o < 2 * NN; o += NTH) {
-        Sa[o] = Qm[o];
-        Sb[o] = Pm[o];
+    if (p.residual_check) {  // double2 copies, 4 in flight per thread
+      const long n2 = NN;  // double2 elements in 2 NN doubles
+      const double2* q2 = reinterpret_cast<const double2*>(Qm);
+      const double2* p2 = reinterpret_cast<const double2*>(Pm);
+      double2* a2 = reinterpret_cast<double2*>(Sa);
+      double2* b2 = reinterpret_cast<double2*>(Sb);
+      for (long o = tid; o < n2; o += 4 * NTH) {
+        double2 vq[4], vp[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const long oo = o + u * NTH;
+          if (oo < n2) {
+            vq[u] = __ldcg(q2 + oo);
+            vp[u] = __ldcg(p2 + oo);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const long oo = o + u * NTH;
+          if (oo < n2) {
+            a2[oo] = vq[u];
+            b2[oo] = vp[u];
+          }
+        }
       }
+    }
   } else {
     A = Sa;
     B = Sb;
@@ -494,22 +525,23 @@ __global__ void __launch_bounds__(NTH, 1) big_gj_kernel(const __grid_constant__ 
       Sb[NN + o] = gqi + pr;
     }
   }
-  for (int c = tid; c < NPMAX; c += NTH) g.used[c] = c >= n;
+  for (int c = tid; c < NPM; c += NTH) g.used[c] = c >= n;
   if (tid == 0) g.fail = 0;
   __syncthreads();
 
   for (int k0 = 0; k0 < n; k0 += GB) {
     const int bs = min(GB, n - k0);
     // (1) panel rows of A; E rows start at zero
+#pragma unroll 4
     for (int w = tid; w < GB * np; w += NTH) {
       const int i = w / np, c = w % np;
       const long o = (long)(k0 + i) * np + c;
-      g.rr[swg(i, c)] = i < bs ? A[o] : 0.0;
-      g.ri[swg(i, c)] = i < bs ? A[NN + o] : 0.0;
+      g.rr[swg(i, c)] = i < bs ? __ldcg(A + o) : 0.0;
+      g.ri[swg(i, c)] = i < bs ? __ldcg(A + NN + o) : 0.0;
       g.mr[swg(i, c)] = 0.0;
       g.mi[swg(i, c)] = 0.0;
     }
-    for (int c = tid; c < NPMAX; c += NTH) g.inpanel[c] = 0;
+    for (int c = tid; c < NPM; c += NTH) g.inpanel[c] = 0;
     __syncthreads();
     // (2) panel factorisation: thread c owns column c of (R; M)
     const int c = tid;
@@ -603,13 +635,28 @@ __global__ void __launch_bounds__(NTH, 1) big_gj_kernel(const __grid_constant__ 
         }
       }
       __syncwarp();
-      for (int cb = 0; cb < np / 8; ++cb) {
+      // X tiles of this row block stream from L2/HBM: a 2-deep register ring
+      // keeps two column blocks in flight ahead of the one being updated
+      const int ncb = np / 8;
+      auto ldx = [&](int cb, double2& xr, double2& xi) {
+        xr = xi = make_double2(0.0, 0.0);
+        if (r < np && cb < ncb) {
+          const long o = (long)r * np + cb * 8 + 2 * (lane & 3);
+          xr = __ldcg(reinterpret_cast<const double2*>(X + o));
+          xi = __ldcg(reinterpret_cast<const double2*>(X + NN + o));
+        }
+      };
+      double2 xr0, xi0, xr1, xi1;
+      ldx(0, xr0, xi0);
+      ldx(1, xr1, xi1);
+      for (int cb = 0; cb < ncb; ++cb) {
         const int cc = cb * 8 + 2 * (lane & 3);
+        const double2 xr = xr0, xi = xi0;
+        xr0 = xr1;
+        xi0 = xi1;
+        ldx(cb + 2, xr1, xi1);
         double d[4] = {0.0, 0.0, 0.0, 0.0};
         if (r < np) {
-          const long o = (long)r * np + cc;
-          const double2 xr = *reinterpret_cast<const double2*>(X + o);
-          const double2 xi = *reinterpret_cast<const double2*>(X + NN + o);
           d[0] = g.inpanel[cc] ? 0.0 : xr.x;
           d[1] = g.inpanel[cc + 1] ? 0.0 : xr.y;
           d[2] = g.inpanel[cc] ? 0.0 : xi.x;
@@ -637,13 +684,14 @@ __global__ void __launch_bounds__(NTH, 1) big_gj_kernel(const __grid_constant__ 
   bool ok = !g.fail;
   // (4) un-permute: result column k is column pc[k] of B; write it into A
   if (ok) {
+#pragma unroll 4
     for (long o = tid; o < NN; o += NTH) {
       const int r = (int)(o / np), k = (int)(o % np);
       double vr = 0.0, vi = 0.0;
       if (k < n && r < n) {
         const long src = (long)r * np + g.pc[k];
-        vr = B[src];
-        vi = B[NN + src];
+        vr = __ldcg(B + src);
+        vi = __ldcg(B + NN + src);
       }
       A[o] = vr;
       A[NN + o] = vi;
@@ -728,6 +776,7 @@ __global__ void __launch_bounds__(NTH, 1) big_gj_kernel(const __grid_constant__ 
     // P <- X, Q <- I
     // rk4: the next step's X2 = Q + h/2 P was formed before the transform
     double* X2m = mx2 >= 0 ? mat(p, pair, mx2) : nullptr;
+#pragma unroll 4
     for (long o = tid; o < NN; o += NTH) {
       const int r = (int)(o / np), c = (int)(o % np);
       const double xr = X[o], xi = X[NN + o];
@@ -795,11 +844,17 @@ cudaError_t big_launch_gj(const BigParams& p, int mode, int step, int mq, int mp
   static bool attr = false;
   if (!attr) {
     cudaError_t e =
-        cudaFuncSetAttribute(big_gj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(GjSmem));
+        cudaFuncSetAttribute(big_gj_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(GjSmem<128>));
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(big_gj_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)sizeof(GjSmem<256>));
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  big_gj_kernel<<<(unsigned)p.npairs, NTH, sizeof(GjSmem), st>>>(p, mode, step, mq, mp, msa, msb, mx2, h);
+  if (p.np <= 128)
+    big_gj_kernel<128><<<(unsigned)p.npairs, NTH, sizeof(GjSmem<128>), st>>>(p, mode, step, mq, mp, msa, msb, mx2, h);
+  else
+    big_gj_kernel<256><<<(unsigned)p.npairs, NTH, sizeof(GjSmem<256>), st>>>(p, mode, step, mq, mp, msa, msb, mx2, h);
   ++*launches;
   return cudaGetLastError();
 }
