@@ -31,7 +31,6 @@ namespace {
 
 constexpr int BM = 64, BN = 32, KC = 16;  // output tile, K chunk
 constexpr int NTH = 256;                  // 8 warps: 4 (rows) x 2 (cols), warp tile 16 x 16
-constexpr int NPMAX = 256;
 
 __device__ __forceinline__ int swp(int k, int c) { return k * BN + (c ^ ((k & 3) << 2)); }
 
@@ -179,26 +178,47 @@ __global__ void __launch_bounds__(NTH, 2) big_stage_kernel(const __grid_constant
 
   // ---- fused epilogue on own elements (row r, cols c, c+1)
   const long NN = (long)np * np;
-  auto ld = [&](int m, long o, double (&v)[4]) {
-    const double* b = mat(p, pair, m);
-    const double2 x = *reinterpret_cast<const double2*>(b + o);
-    const double2 y = *reinterpret_cast<const double2*>(b + NN + o);
-    v[0] = x.x;
-    v[1] = x.y;
-    v[2] = y.x;
-    v[3] = y.y;
-  };
   auto st = [&](int m, long o, const double (&v)[4]) {
     double* b = mat(p, pair, m);
     *reinterpret_cast<double2*>(b + o) = make_double2(v[0], v[1]);
     *reinterpret_cast<double2*>(b + NN + o) = make_double2(v[2], v[3]);
   };
   const double* g2a = p.gamma2 + pair * n;
+  // the rk4 stages' extra operands (X2 | SQ, and W): per row block, loaded
+  // for both column blocks before any arithmetic or store so the latencies
+  // overlap (a full prefetch of all four blocks would spill)
+  const int ma = s.kind == 3 ? s.mx2 : (s.kind >= 4 ? s.msq : -1);
+  const int mw = (s.kind == 4 || s.kind == 6) ? s.mw : -1;
+  const double* pa = ma >= 0 ? mat(p, pair, ma) : nullptr;
+  const double* pw = mw >= 0 ? mat(p, pair, mw) : nullptr;
 #pragma unroll
   for (int mb = 0; mb < 2; ++mb) {
     const int r = r0 + wm * 16 + mb * 8 + (lane >> 2);
     if (r >= np) continue;
     const double g2 = r < n ? g2a[r] : 0.0;
+    double ea[2][4], eb[2][4];
+#pragma unroll
+    for (int nb = 0; nb < 2; ++nb) {
+      const int c = c0 + wn * 16 + nb * 8 + 2 * (lane & 3);
+      const long o = (long)r * np + c;
+      double2 a0 = make_double2(0.0, 0.0), a1 = a0, w0 = a0, w1 = a0;
+      if (c < np && pa) {
+        a0 = __ldcg(reinterpret_cast<const double2*>(pa + o));
+        a1 = __ldcg(reinterpret_cast<const double2*>(pa + NN + o));
+      }
+      if (c < np && pw) {
+        w0 = __ldcg(reinterpret_cast<const double2*>(pw + o));
+        w1 = __ldcg(reinterpret_cast<const double2*>(pw + NN + o));
+      }
+      ea[nb][0] = a0.x;
+      ea[nb][1] = a0.y;
+      ea[nb][2] = a1.x;
+      ea[nb][3] = a1.y;
+      eb[nb][0] = w0.x;
+      eb[nb][1] = w0.y;
+      eb[nb][2] = w1.x;
+      eb[nb][3] = w1.y;
+    }
 #pragma unroll
     for (int nb = 0; nb < 2; ++nb) {
       const int c = c0 + wn * 16 + nb * 8 + 2 * (lane & 3);
@@ -246,7 +266,8 @@ __global__ void __launch_bounds__(NTH, 2) big_stage_kernel(const __grid_constant
         double pv[4] = {pe[0], pe[1], pe[2], pe[3]}, sq[4], w[4];
         if (s.kind == 3) {  // X = Q: SQ = K1, X3 = X2 + h^2/4 K1, W = Q + hP, P += h/6 K1
           double x2[4];
-          ld(s.mx2, o, x2);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) x2[q] = ea[nb][q];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             sq[q] = K[q];
@@ -258,8 +279,11 @@ __global__ void __launch_bounds__(NTH, 2) big_stage_kernel(const __grid_constant
           st(s.mx3, o, x2);
           st(s.mw, o, w);
         } else if (s.kind == 4) {  // X = X2: SQ += K2, P += h/3 K2, V = W + h^2/2 K2
-          ld(s.msq, o, sq);
-          ld(s.mw, o, w);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            sq[q] = ea[nb][q];
+            w[q] = eb[nb][q];
+          }
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             sq[q] += K[q];
@@ -269,7 +293,8 @@ __global__ void __launch_bounds__(NTH, 2) big_stage_kernel(const __grid_constant
           st(s.msq, o, sq);
           st(s.mv, o, w);
         } else if (s.kind == 5) {  // X = X3: SQ += K3, P += h/3 K3
-          ld(s.msq, o, sq);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) sq[q] = ea[nb][q];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             sq[q] += K[q];
@@ -277,8 +302,11 @@ __global__ void __launch_bounds__(NTH, 2) big_stage_kernel(const __grid_constant
           }
           st(s.msq, o, sq);
         } else {  // kind 6, X = X4 (V): P += h/6 K4, Q = W + h^2/6 SQ, X2 = Q + h/2 P
-          ld(s.msq, o, sq);
-          ld(s.mw, o, w);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            sq[q] = ea[nb][q];
+            w[q] = eb[nb][q];
+          }
           double qn[4], x2[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
