@@ -414,6 +414,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
   double* g2s = reinterpret_cast<double*>(fv + 2 * NP);  // [NP]
   // Gershgorin row sums alias the Gauss-Jordan multipliers (never live together)
   static_assert(C::WN <= 2, "rsum/dsum alias fv");
+  static_assert(sizeof(PanelScratch) >= 2 * C::WN * NP * sizeof(double), "rsum/dsum alias the panel scratch");
   double* rsum = reinterpret_cast<double*>(fv);  // [WN][NP]
   double* dsum = rsum + C::WN * NP;              // [WN][NP]
   int* soff = reinterpret_cast<int*>(g2s + NP);  // [NP]
@@ -782,7 +783,13 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
     PROF_MARK(2);
     double* Sr = RK4 ? Xr[1] : Nr;  // free scratch plane pair
     double* Si = RK4 ? Xi[1] : Ni;
-    const double xi = finite_and_gershgorin<C>(Ar, Ai, P, own, n, rsum, dsum, *sc, tid, warp, lane);
+    // row-sum buffers alternate by step (the Gauss-Jordan multipliers / the
+    // blocked solve's panel scratch, both idle here): the check has one
+    // CTA-wide barrier, and a warp still folding step k's sums must not see
+    // a column group of step k+1 overwrite them
+    double* const rsb = (step & 1) ? reinterpret_cast<double*>(ps) : rsum;
+    const double xi =
+        finite_and_gershgorin<C>(Ar, Ai, P, own, n, rsb, rsb + (dsum - rsum), *sc, tid, warp, lane);
     PROF_MARK(4);
     if (xi < 0.0) {
       code = 1;
