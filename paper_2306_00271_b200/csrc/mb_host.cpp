@@ -461,24 +461,6 @@ void free_plan(mb_plan* pl) {
   delete pl;
 }
 
-mb_rods rods_view(const RodTables& t, std::vector<double>& k, std::vector<int>& m, std::vector<double>& diff,
-                  std::vector<int>& dm) {
-  for (const Rod& r : t.rods) {
-    k.push_back(r.k.x);
-    k.push_back(r.k.y);
-    m.push_back(r.m1);
-    m.push_back(r.m2);
-  }
-  for (std::size_t d = 0; d < t.diff.size(); ++d) {
-    diff.push_back(t.diff[d].x);
-    diff.push_back(t.diff[d].y);
-    dm.push_back(t.diff_m[d].first);
-    dm.push_back(t.diff_m[d].second);
-  }
-  return mb_rods{(int)t.rods.size(), k.data(), m.data(), (int)t.diff.size(), diff.data(), dm.data(),
-                 t.diff_index.data()};
-}
-
 mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* fields, int nfields, double gamma,
                      const mb_pair* pairs, long npairs, const mb_stepper* stepper, const mb_options* opts) {
   if (!ctx || !rods || !fields || !pairs || !stepper || !opts) fail(MB_ERR_ARG, "null argument");
