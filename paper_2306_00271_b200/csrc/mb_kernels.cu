@@ -242,7 +242,15 @@ __device__ __forceinline__ void tile_k8(double (&c)[4], const double* Ar, const 
   }
 }
 
-template <class C>
+// VERIFY: used when the Gershgorin estimate is not finite. Partial pivoting
+// may then leave the diagonal, but it rarely does (cfg1: 45 of the 50
+// non-dominant RHSTs per point keep every pivot on the diagonal; cfg2: all).
+// Warp 0 replays each panel's eliminations on the panel's full rows and
+// checks the pivot rule of the unblocked elimination at every step: the
+// diagonal must be a first maximum of |a_kj|^2 over j >= k. The first failed
+// check (or zero pivot) returns false, and the caller redoes the solve with
+// partial pivoting from the saved Q and P.
+template <class C, bool VERIFY = false>
 __device__ bool gauss_jordan_dominant(double* Ar, double* Ai, double* Br, double* Bi, int n, PanelScratch& ps,
                                       int tid, int warp, int lane) {
   constexpr int NP = C::NP;
@@ -261,6 +269,64 @@ __device__ bool gauss_jordan_dominant(double* Ar, double* Ai, double* Br, double
     // (2) warp 0: T = A_pp^-1 (row-operation Gauss-Jordan on [A_pp | I]; the
     // padded block of a partial panel is the identity)
     if (warp == 0) {
+      int bad = 0;
+      if constexpr (VERIFY) {
+        constexpr int NQ = (NP + 31) / 32;
+        double2 R[8][NQ];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) {
+            const int j = lane + 32 * q;
+            R[i][q] = (i < bsz && j < NP) ? make_double2(Ar[sw<NP>(k0 + i, j)], Ai[sw<NP>(k0 + i, j)])
+                                          : make_double2(0.0, 0.0);
+          }
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          if (t >= bsz) break;
+          const int k = k0 + t;
+          double vmax = 0.0, vkk = 0.0;
+          double2 rk = make_double2(0.0, 0.0);
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) {
+            const int j = lane + 32 * q;
+            const double v = R[t][q].x * R[t][q].x + R[t][q].y * R[t][q].y;
+            if (j > k && j < n) vmax = fmax(vmax, v);
+            if (q == (k >> 5)) {
+              vkk = v;
+              rk = R[t][q];
+            }
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) vmax = fmax(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+          vkk = __shfl_sync(0xffffffffu, vkk, k & 31);
+          rk = make_double2(__shfl_sync(0xffffffffu, rk.x, k & 31), __shfl_sync(0xffffffffu, rk.y, k & 31));
+          bad |= !(vkk >= vmax && vkk > 0.0);  // NaN fails too
+          double r;
+          asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(vkk));
+          r = r * fma(-vkk, r, 2.0);
+          r = r * fma(-vkk, r, 2.0);
+          const double2 inv = make_double2(rk.x * r, -rk.y * r);
+#pragma unroll
+          for (int i = t + 1; i < 8; ++i) {
+            if (i >= bsz) break;
+            double2 xi = R[i][0];
+#pragma unroll
+            for (int q = 1; q < NQ; ++q)
+              if (q == (k >> 5)) xi = R[i][q];
+            xi = make_double2(__shfl_sync(0xffffffffu, xi.x, k & 31), __shfl_sync(0xffffffffu, xi.y, k & 31));
+            const double2 x = cmul(xi, inv);
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+              const int j = lane + 32 * q;
+              const double2 f = R[t][q];
+              const double2 nv =
+                  make_double2(R[i][q].x - (f.x * x.x - f.y * x.y), R[i][q].y - (f.x * x.y + f.y * x.x));
+              R[i][q] = (j == k) ? x : nv;
+            }
+          }
+        }
+      }
       const int col = lane & 15;  // lanes 0..7: A_pp columns, 8..15: identity columns
       double2 v[8];
 #pragma unroll
@@ -273,7 +339,6 @@ __device__ bool gauss_jordan_dominant(double* Ar, double* Ai, double* Br, double
           v[i] = make_double2(i == col - 8 ? 1.0 : 0.0, 0.0);
         }
       }
-      int bad = 0;
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
         const double2 piv = make_double2(__shfl_sync(0xffffffffu, v[t].x, t), __shfl_sync(0xffffffffu, v[t].y, t));
@@ -800,9 +865,10 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
       // P <- P Q^-1, Q <- I (proposed.cpp:196-202)
       double* Or = Xr[2];  // saved Q for the residual gate
       double* Oi = Xi[2];
+      const bool dominant = isfinite(xi);
       FOR_BLK {
         double v[4];
-        if (p.residual_check) {
+        if (p.residual_check || !dominant) {  // saved Q: residual gate, pivoting fallback
           own.ld(Ar, Ai, mb, nb, v);
           own.st(Or, Oi, mb, nb, v);
         }
@@ -811,17 +877,29 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
       __syncthreads();
       PROF_MARK(5);
       // finite estimate = strict row dominance: pivot-free blocked solve
-      // (identical pivot sequence); otherwise partial pivoting
+      // (identical pivot sequence). Otherwise the same blocked solve with the
+      // pivot rule checked panel by panel, and partial pivoting from the
+      // saved Q and P when a pivot would leave the diagonal.
       bool ok;
-      if (isfinite(xi)) {
+      if (dominant) {
         ok = gauss_jordan_dominant<C>(Ar, Ai, Sr, Si, n, *ps, tid, warp, lane);
       } else {
+        ok = gauss_jordan_dominant<C, true>(Ar, Ai, Sr, Si, n, *ps, tid, warp, lane);
+        if (!ok) {
+          FOR_BLK {
+            double v[4];
+            own.ld(Or, Oi, mb, nb, v);
+            own.st(Ar, Ai, mb, nb, v);
+            own.st(Sr, Si, mb, nb, P[mb][nb]);
+          }
+          __syncthreads();
 #ifdef MB_PROFILE
-        ok = gauss_jordan<C, RK4 ? 4 : 0>(Ar, Ai, Sr, Si, fv, n, *sc, warp, lane, tid == 0 ? prof_acc : nullptr);
-        prof_t = clock64();
+          ok = gauss_jordan<C, RK4 ? 4 : 0>(Ar, Ai, Sr, Si, fv, n, *sc, warp, lane, tid == 0 ? prof_acc : nullptr);
+          prof_t = clock64();
 #else
-        ok = gauss_jordan<C, RK4 ? 4 : 0>(Ar, Ai, Sr, Si, fv, n, *sc, warp, lane);
+          ok = gauss_jordan<C, RK4 ? 4 : 0>(Ar, Ai, Sr, Si, fv, n, *sc, warp, lane);
 #endif
+        }
       }
       PROF_MARK(3);
       if (ok && p.residual_check)
