@@ -458,6 +458,8 @@ struct GjSmem {
   double rr[GB * NPM], ri[GB * NPM];  // panel rows of A (column ops applied)
   double mr[GB * NPM], mi[GB * NPM];  // rows of E at the panel's pivot columns
   double2 colp[2 * GB];
+  double2 colq[2][2 * GB];  // diagonal-pivot pass: normalised pivot column, by step parity
+  double pv2[2];            // |pivot|^2, by step parity
   double red_v[NTH / 32];
   int red_j[NTH / 32];
   int pc[NPM];           // pivot column of row k
@@ -571,52 +573,31 @@ __global__ void __launch_bounds__(NTH, NPM == 128 ? 2 : 1) big_gj_kernel(const _
     }
     for (int c = tid; c < NPM; c += NTH) g.inpanel[c] = 0;
     __syncthreads();
-    // (2) panel factorisation: thread c owns column c of (R; M)
+    // (2) panel factorisation: thread c owns column c of (R; M).
+    // (2a) diagonal pivots, verified: most panels keep every partial-pivoting
+    // pivot on the diagonal, and then the pivot search is only a check. Each
+    // thread compares its own column's |a_tc|^2 with the diagonal's, so a step
+    // needs one barrier (the pivot column, double-buffered by step parity)
+    // instead of three. A diagonal that would lose to a later column (first
+    // maximum wins), a zero pivot or an already-used diagonal column reloads
+    // the panel and runs (2b), the pivoting factorisation.
     const int c = tid;
+    bool marked = false;
+    int myfail = 0;
     for (int t = 0; t < bs; ++t) {
-      double v = -1.0;
-      if (c < np && !g.used[c]) {
-        const double a = g.rr[swg(t, c)], b = g.ri[swg(t, c)];
-        v = a * a + b * b;
-      }
-      int j = c;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, v, o);
-        const int oj = __shfl_xor_sync(0xffffffffu, j, o);
-        if (ov > v || (ov == v && oj < j)) {
-          v = ov;
-          j = oj;
-        }
-      }
-      if (lane == 0) {
-        g.red_v[warp] = v;
-        g.red_j[warp] = j;
-      }
-      __syncthreads();
-      if (tid == 0) {
-        double bv = g.red_v[0];
-        int bj = g.red_j[0];
-        for (int w = 1; w < NTH / 32; ++w)
-          if (g.red_v[w] > bv || (g.red_v[w] == bv && g.red_j[w] < bj)) {
-            bv = g.red_v[w];
-            bj = g.red_j[w];
-          }
-        g.piv = bj;
-        g.pivval = bv;
-      }
-      __syncthreads();
-      if (!(g.pivval > 0.0)) {
-        if (tid == 0) g.fail = 1;
-        break;
-      }
-      const int ct = g.piv;
+      const int ct = k0 + t, buf = t & 1;
       if (c == ct) {
-        g.used[c] = 1;
+        const double2 pv = make_double2(g.rr[swg(t, c)], g.ri[swg(t, c)]);
+        const double m2 = pv.x * pv.x + pv.y * pv.y;
+        if (g.used[c] || !(m2 > 0.0)) myfail = 1;
+        if (!g.used[c]) {
+          g.used[c] = 1;
+          marked = true;
+        }
         g.inpanel[c] = 1;
         g.pc[k0 + t] = c;
+        g.pv2[buf] = m2;
         g.mr[swg(t, c)] = 1.0;  // row c of E is e_c until now
-        const double2 pv = make_double2(g.rr[swg(t, c)], g.ri[swg(t, c)]);
         const double2 inv = cinv(pv);
         for (int i = 0; i < GB; ++i) {
           const double2 x = cmul(make_double2(g.rr[swg(i, c)], g.ri[swg(i, c)]), inv);
@@ -625,19 +606,106 @@ __global__ void __launch_bounds__(NTH, NPM == 128 ? 2 : 1) big_gj_kernel(const _
           g.ri[swg(i, c)] = x.y;
           g.mr[swg(i, c)] = y.x;
           g.mi[swg(i, c)] = y.y;
-          g.colp[i] = x;
-          g.colp[GB + i] = y;
+          g.colq[buf][i] = x;
+          g.colq[buf][GB + i] = y;
         }
       }
-      __syncthreads();
+      if (__syncthreads_or(myfail)) break;
       if (c < np && c != ct) {
         const double2 f = make_double2(g.rr[swg(t, c)], g.ri[swg(t, c)]);
+        // the unblocked search takes the first maximum over the unused
+        // columns: a later column must not beat the diagonal, an earlier
+        // one (left unused by a pivoting panel) must not tie it
+        const double vc = f.x * f.x + f.y * f.y;
+        if (!g.used[c] && (vc > g.pv2[buf] || (c < ct && vc == g.pv2[buf]))) myfail = 1;
         for (int i = 0; i < GB; ++i) {
-          const double2 x = g.colp[i], y = g.colp[GB + i];
+          const double2 x = g.colq[buf][i], y = g.colq[buf][GB + i];
           g.rr[swg(i, c)] -= f.x * x.x - f.y * x.y;
           g.ri[swg(i, c)] -= f.x * x.y + f.y * x.x;
           g.mr[swg(i, c)] -= f.x * y.x - f.y * y.y;
           g.mi[swg(i, c)] -= f.x * y.y + f.y * y.x;
+        }
+      }
+    }
+    if (__syncthreads_or(myfail)) {
+      // (2b) partial pivoting from the reloaded panel
+      if (marked) g.used[c] = 0;
+      for (int w = tid; w < GB * np; w += NTH) {
+        const int i = w / np, cc = w % np;
+        const long o = (long)(k0 + i) * np + cc;
+        g.rr[swg(i, cc)] = i < bs ? __ldcg(A + o) : 0.0;
+        g.ri[swg(i, cc)] = i < bs ? __ldcg(A + NN + o) : 0.0;
+        g.mr[swg(i, cc)] = 0.0;
+        g.mi[swg(i, cc)] = 0.0;
+      }
+      for (int cc = tid; cc < NPM; cc += NTH) g.inpanel[cc] = 0;
+      __syncthreads();
+    for (int t = 0; t < bs; ++t) {
+        double v = -1.0;
+        if (c < np && !g.used[c]) {
+          const double a = g.rr[swg(t, c)], b = g.ri[swg(t, c)];
+          v = a * a + b * b;
+        }
+        int j = c;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+          const int oj = __shfl_xor_sync(0xffffffffu, j, o);
+          if (ov > v || (ov == v && oj < j)) {
+            v = ov;
+            j = oj;
+          }
+        }
+        if (lane == 0) {
+          g.red_v[warp] = v;
+          g.red_j[warp] = j;
+        }
+        __syncthreads();
+        if (tid == 0) {
+          double bv = g.red_v[0];
+          int bj = g.red_j[0];
+          for (int w = 1; w < NTH / 32; ++w)
+            if (g.red_v[w] > bv || (g.red_v[w] == bv && g.red_j[w] < bj)) {
+              bv = g.red_v[w];
+              bj = g.red_j[w];
+            }
+          g.piv = bj;
+          g.pivval = bv;
+        }
+        __syncthreads();
+        if (!(g.pivval > 0.0)) {
+          if (tid == 0) g.fail = 1;
+          break;
+        }
+        const int ct = g.piv;
+        if (c == ct) {
+          g.used[c] = 1;
+          g.inpanel[c] = 1;
+          g.pc[k0 + t] = c;
+          g.mr[swg(t, c)] = 1.0;  // row c of E is e_c until now
+          const double2 pv = make_double2(g.rr[swg(t, c)], g.ri[swg(t, c)]);
+          const double2 inv = cinv(pv);
+          for (int i = 0; i < GB; ++i) {
+            const double2 x = cmul(make_double2(g.rr[swg(i, c)], g.ri[swg(i, c)]), inv);
+            const double2 y = cmul(make_double2(g.mr[swg(i, c)], g.mi[swg(i, c)]), inv);
+            g.rr[swg(i, c)] = x.x;
+            g.ri[swg(i, c)] = x.y;
+            g.mr[swg(i, c)] = y.x;
+            g.mi[swg(i, c)] = y.y;
+            g.colp[i] = x;
+            g.colp[GB + i] = y;
+          }
+        }
+        __syncthreads();
+        if (c < np && c != ct) {
+          const double2 f = make_double2(g.rr[swg(t, c)], g.ri[swg(t, c)]);
+          for (int i = 0; i < GB; ++i) {
+            const double2 x = g.colp[i], y = g.colp[GB + i];
+            g.rr[swg(i, c)] -= f.x * x.x - f.y * x.y;
+            g.ri[swg(i, c)] -= f.x * x.y + f.y * x.x;
+            g.mr[swg(i, c)] -= f.x * y.x - f.y * y.y;
+            g.mi[swg(i, c)] -= f.x * y.y + f.y * y.x;
+          }
         }
       }
     }
