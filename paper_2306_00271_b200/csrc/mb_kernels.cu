@@ -221,6 +221,7 @@ struct PanelScratch {
   double rr[8 * 64], ri[8 * 64];  // -A[panel rows][:] with the panel columns zeroed
   double tr[64], ti[64];          // T = A_pp^-1, row-major [k][n]
   int fail;
+  int vfail;  // VERIFY: a pivot would leave the diagonal
 };
 
 // 8x8 complex tile product: c += A[r0.., k0..k0+7] (swizzled NP plane) x
@@ -268,9 +269,11 @@ __device__ bool gauss_jordan_dominant(double* Ar, double* Ai, double* Br, double
     }
     // (2) warp 0: T = A_pp^-1 (row-operation Gauss-Jordan on [A_pp | I]; the
     // padded block of a partial panel is the identity)
-    if (warp == 0) {
+    // the pivot-rule replay (VERIFY) runs on warp 1 next to warp 0's inverse
+    constexpr int VW = C::NW > 1 ? 1 : 0;
+    if (VERIFY && warp == VW) {
       int bad = 0;
-      if constexpr (VERIFY) {
+      {
         constexpr int NQ = (NP + 31) / 32;
         double2 R[8][NQ];
 #pragma unroll
@@ -327,6 +330,10 @@ __device__ bool gauss_jordan_dominant(double* Ar, double* Ai, double* Br, double
           }
         }
       }
+      if (lane == 0) ps.vfail = bad;
+    }
+    if (warp == 0) {
+      int bad = 0;
       const int col = lane & 15;  // lanes 0..7: A_pp columns, 8..15: identity columns
       double2 v[8];
 #pragma unroll
@@ -372,7 +379,7 @@ __device__ bool gauss_jordan_dominant(double* Ar, double* Ai, double* Br, double
       if (lane == 0) ps.fail = bad;
     }
     __syncthreads();
-    if (ps.fail) return false;
+    if (ps.fail || (VERIFY && ps.vfail)) return false;
     // (3)+(4): whole 8-row blocks per warp: A rows >= k0+8 (future panels),
     // B rows < n
     const int nbA = (NP - k0 - 8) >> 3;
