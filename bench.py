@@ -107,7 +107,7 @@ def fp64_peak():
         return 37.1, "fallback 37.1 TF/s (own DMMA measurement, round 1)"
 
 
-NCU_SUMMARY = "ncu_summary_r01y.json"  # the latest committed capture of the bench command
+NCU_SUMMARY = "ncu_summary_r01ab.json"  # the latest committed capture of the bench command
 
 
 def hbm_peak():
