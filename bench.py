@@ -322,7 +322,13 @@ def main():
                                    "frac": pot_bytes / (pot / args.steps * 1e-3) / 1e9 / hbm_peak()[0],
                                    "bytes_per_launch": pot_bytes,
                                    "bytes_rule": "16 B x structures x node slots x ndiff (coefficient table write)",
-                                   "note": "K1 is ~0.1% of the step; at cfg1 it is bound by its exp() evaluations"},
+                                   # each 16-byte output sums T = 4 x atoms complex x real terms:
+                                   # 8T flops, so FP64 caps K1 at peak_flops / (8T) x 16 B
+                                   "compute_ceiling_gbs": peak * 1e12 / (8.0 * 4 * max(len(s.species) for s in w.structures)) * 16 / 1e9,
+                                   "frac_of_compute_ceiling": (pot_bytes / (pot / args.steps * 1e-3) / 1e9) / (
+                                       peak * 1e12 / (8.0 * 4 * max(len(s.species) for s in w.structures)) * 16 / 1e9),
+                                   "note": "K1 is ~0.1% of the step; with T = 4 x atoms terms per output it is "
+                                           "FP64-compute-bound below the HBM peak (compute_ceiling_gbs)"},
             "cpu_baseline": cb, "e2e": e2e, "gpu_launches": launches,
             "kernel_ms": {"potential": pot / args.steps, "propagate": ms_prop},
             "rhst_per_point": rhst_mean, "rhst_pivoting_per_point": rhst_piv, "wall_s_timed": t_wall, "clocks": ck,
