@@ -1,0 +1,542 @@
+// ORACLE — TEST INFRASTRUCTURE ONLY. Python bindings of the REFERENCE itself:
+// the hot-path sources under /root/reference/proj/core/src are compiled
+// verbatim (oracle/Makefile target `ref`, outputs in oracle/_ref/) against the
+// Eigen-subset shim in oracle/ref/shim, and this file exposes them to pytest,
+// tests/golden/make_golden.py and bench.py's CPU legs with the same Python
+// surface as the restatement (oracle/mb_oracle_py.cpp), so either can be the
+// checker.
+//
+// Only the BASELINE extensions the reference lacks are added here, each
+// outside the reference's code:
+//   * RodSet.build_first(lattice, n): the reference's own RodSet::build at a
+//     cutoff that holds >= n rods, truncated to its first n rods (the
+//     reference's sort order is total, rods.cpp:58-63) and the difference
+//     table rebuilt exactly as rods.cpp:75-94 does. The private members are
+//     reached through the explicit-instantiation access rule, not by editing
+//     the reference.
+//   * PotentialField.atoms(...): the SURVEY §8a row P0 atom potential (not in
+//     the reference) is evaluated by the restatement (oracle/mb_oracle.cpp,
+//     BoundPotential Kind::Atoms) at every node height the reference will ask
+//     for, and handed to the reference as a Tabulated field on exactly those
+//     heights. The reference's cubic Hermite rule is exact at its grid nodes
+//     (potential.cpp:189-197: t = 0 or 1 there), so the reference propagates
+//     the atom potential itself. Bulk-period heights are added after the
+//     reference's map_z (potential.cpp:152-167, restated bit for bit below).
+//   * solve_rows(...): sweep.cpp:89-109's per-row body (BeamGeometry,
+//     GammaMatrix, bulk seed, solve_proposed with the shared UTable) with
+//     SolveStats and rho kept, over the same atomic-counter thread pool
+//     (sweep.cpp:111-138). rocking_curve(...) calls the reference's own
+//     manybeam::rocking_curve unchanged (eta only).
+#include <pybind11/numpy.h>
+#include <pybind11/pybind11.h>
+#include <pybind11/stl.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <exception>
+#include <map>
+#include <memory>
+#include <optional>
+#include <thread>
+#include <vector>
+
+#include "manybeam/conventional.hpp"
+#include "manybeam/curve.hpp"
+#include "manybeam/geometry.hpp"
+#include "manybeam/kernels.hpp"
+#include "manybeam/potential.hpp"
+#include "manybeam/proposed.hpp"
+#include "manybeam/rods.hpp"
+#include "manybeam/slicing.hpp"
+#include "manybeam/stages.hpp"
+#include "manybeam/sweep.hpp"
+#include "mb_oracle.hpp"
+
+namespace py = pybind11;
+namespace mb = manybeam;
+using cd = std::complex<double>;
+
+// ------------------------------------------------------------ private access
+// [temp.explicit]/12: access checking does not apply to the names in an
+// explicit instantiation, so a member pointer to a private member can be
+// captured without touching the reference's headers.
+template <class Tag, typename Tag::type M>
+struct Rob {
+  friend typename Tag::type get(Tag) { return M; }
+};
+#define MB_ROB(NAME, TYPE, MEMBER)                      \
+  struct NAME {                                         \
+    using type = TYPE mb::RodSet::*;                    \
+    friend type get(NAME);                              \
+  };                                                    \
+  template struct Rob<NAME, &mb::RodSet::MEMBER>;
+MB_ROB(RodK, std::vector<mb::Vec2>, k_)
+MB_ROB(RodM, std::vector<Eigen::Vector2i>, m_)
+MB_ROB(RodDiff, std::vector<mb::Vec2>, diff_)
+MB_ROB(RodDiffM, std::vector<Eigen::Vector2i>, diff_m_)
+MB_ROB(RodDiffIndex, std::vector<int>, diff_index_)
+MB_ROB(RodCutoff, double, cutoff_)
+
+namespace {
+
+// EXTENSION: first n rods of the reference order.
+mb::RodSet rods_first(const mb::Lattice2D& lat, int n) {
+  lat.validate();
+  if (n < 1) throw mb::ConfigError("rod count must be >= 1");
+  const double bmin = std::min(lat.b1().norm(), lat.b2().norm());
+  double cutoff = 0.5 * bmin;
+  mb::RodSet rs = mb::RodSet::build(lat, cutoff);
+  while (rs.size() < n) {
+    cutoff *= 1.25;
+    rs = mb::RodSet::build(lat, cutoff);
+  }
+  auto& k = rs.*get(RodK{});
+  auto& m = rs.*get(RodM{});
+  k.resize((std::size_t)n);
+  m.resize((std::size_t)n);
+  rs.*get(RodCutoff{}) = k.back().norm();
+  // difference table of the truncated set: rods.cpp:75-94
+  auto& diff = rs.*get(RodDiff{});
+  auto& diff_m = rs.*get(RodDiffM{});
+  auto& diff_index = rs.*get(RodDiffIndex{});
+  diff.clear();
+  diff_m.clear();
+  const mb::Vec2 b1 = lat.b1(), b2 = lat.b2();
+  std::map<std::pair<int, int>, int> seen;
+  diff_index.assign((std::size_t)n * n, -1);
+  for (int j = 0; j < n; ++j)
+    for (int q = 0; q < n; ++q) {
+      const Eigen::Vector2i dm = m[j] - m[q];
+      auto key = std::make_pair(dm.x(), dm.y());
+      auto it = seen.find(key);
+      int d;
+      if (it == seen.end()) {
+        d = (int)diff.size();
+        seen.emplace(key, d);
+        diff.push_back(dm.x() * b1 + dm.y() * b2);
+        diff_m.push_back(dm);
+      } else {
+        d = it->second;
+      }
+      diff_index[(std::size_t)j * n + q] = d;
+    }
+  return rs;
+}
+
+// A field as the tests hand it over: either a reference PotentialField, or the
+// atom model (EXTENSION) that is tabulated per solve on the node heights.
+struct RefField {
+  std::optional<mb::PotentialField> direct;
+  std::optional<mbo::PotentialField> atoms;
+  double z_bottom = -1.0;
+  std::optional<double> bulk_period;
+};
+
+// potential.cpp:152-167 restated bit for bit (same operations, same order).
+double map_z_bulk(double z, double zb, double p) {
+  constexpr double kZTol = 1e-9;
+  if (z > 0.0) z = 0.0;
+  if (z >= zb) return z;
+  if (z >= zb - kZTol) return zb;
+  const double k = std::ceil((zb - z) / p - 1e-12);
+  double zm = z + k * p;
+  if (zm < zb) zm += p;
+  if (zm > zb + p) zm = zb + p;
+  return std::min(zm, 0.0);
+}
+
+void collect_nodes(const mb::StepWindow& w, const mb::NodeSchedule& s, std::vector<double>& out) {
+  for (long i = 0; i < w.count; ++i)
+    for (int m = 0; m < s.nodes(); ++m) out.push_back(mb::node_z(w, i, m, s));
+}
+
+// Materialise the reference field for one solve configuration.
+mb::PotentialField realise(const RefField& f, const mb::RodSet& rods, const mb::SlicingPlan& plan,
+                           const mb::StepperSpec& spec, double dz, int threads) {
+  if (f.direct) return *f.direct;
+  const mb::NodeSchedule sched = mb::schedule_for(spec);
+  std::vector<double> zs;
+  collect_nodes(mb::StepWindow::of_plan(plan), sched, zs);
+  if (f.bulk_period) {
+    // the bulk window of compute_bulk_reflection_proposed (proposed.cpp:318-321)
+    const double p = *f.bulk_period, ze = f.z_bottom;
+    const long L = std::max(1L, std::lround(p / dz));
+    std::vector<double> zb;
+    collect_nodes(mb::StepWindow::over(ze - p, ze, L), sched, zb);
+    for (double z : zb) zs.push_back(map_z_bulk(z, ze, p));
+  }
+  std::sort(zs.begin(), zs.end());
+  zs.erase(std::unique(zs.begin(), zs.end()), zs.end());
+
+  // atom coefficients at every height, by the restatement (the P0 formula is
+  // builder-defined; the reference has no atom model)
+  const auto& lat = rods.lattice();
+  mbo::Lattice2D ol;
+  ol.a1 = mbo::Vec2{lat.a1.x(), lat.a1.y()};
+  ol.a2 = mbo::Vec2{lat.a2.x(), lat.a2.y()};
+  const mbo::RodSet orods = mbo::RodSet::build_first(ol, rods.size());
+  mbo::PotentialField af = *f.atoms;
+  af.bulk_period.reset();  // heights are already mapped into [z_bottom, 0]
+  const mbo::BoundPotential bound(af, orods);
+  const int nd = orods.diff_count();
+  std::vector<mb::TabulatedEntry> entries((std::size_t)nd);
+  for (int d = 0; d < nd; ++d) {
+    entries[d].dm = Eigen::Vector2i(orods.diff_m[d].x, orods.diff_m[d].y);
+    entries[d].values.resize(zs.size());
+  }
+  const int nt = std::max(1, std::min<int>(threads, (int)zs.size()));
+  std::atomic<std::size_t> next{0};
+  std::vector<std::thread> pool;
+  for (int t = 0; t < nt; ++t)
+    pool.emplace_back([&] {
+      std::vector<cd> c;
+      for (;;) {
+        const std::size_t i = next.fetch_add(1);
+        if (i >= zs.size()) return;
+        bound.eval_coeffs(zs[i], c);
+        for (int d = 0; d < nd; ++d) entries[d].values[i] = c[d];
+      }
+    });
+  for (auto& th : pool) th.join();
+  return mb::PotentialField::tabulated(f.z_bottom, zs, std::move(entries), f.bulk_period);
+}
+
+struct Opts {
+  std::string method = "rk4";
+  double dz = 0.01;
+  long slices = 0;  // > 0: require that dz reproduces exactly this count
+  double rhst_threshold = 1000.0;
+  int threads = 1;
+  std::size_t table_budget_bytes = (std::size_t)1 << 30;
+  // custom splitting stepper (StepperSpec::splitting, proposed.hpp:35-36)
+  std::optional<mb::StepperSpec> stepper;
+};
+
+const mb::StepperSpec& spec_of(const Opts& o) { return o.stepper ? *o.stepper : mb::StepperSpec::by_name(o.method); }
+
+mb::SlicingPlan plan_of(const RefField& f, const Opts& o) {
+  const mb::SlicingPlan plan = mb::SlicingPlan::with_target_dz(f.z_bottom, o.dz);
+  if (o.slices > 0 && plan.count != o.slices)
+    throw mb::ConfigError("mb_ref: dz does not reproduce the requested slice count");
+  return plan;
+}
+
+int thread_count(int threads, long rows) {
+  if (threads <= 0) threads = (int)std::max(1u, std::thread::hardware_concurrency());
+  return (int)std::max<long>(1, std::min<long>(threads, rows));
+}
+
+struct Rows {
+  long rows = 0, n = 0;
+  std::vector<double> eta;
+  std::vector<cd> rho;
+  std::vector<long> rhst;
+  double solve_seconds = 0.0;
+};
+
+// sweep.cpp:54-143 with the per-row body of :89-109, keeping rho and SolveStats.
+Rows solve_rows(const RefField& field, const mb::RodSet& rods, double gamma, const mb::AngleGrid& grid,
+                const Opts& o) {
+  const auto t0 = std::chrono::steady_clock::now();
+  const mb::StepperSpec& spec = spec_of(o);
+  const mb::SlicingPlan plan = plan_of(field, o);
+  const mb::PotentialField pf = realise(field, rods, plan, spec, o.dz, thread_count(o.threads, 1 << 20));
+  const mb::BoundPotential bound(pf, rods);
+  const long rows = grid.rows();
+  const int n = rods.size();
+  const mb::NodeSchedule sched = mb::schedule_for(spec);
+  std::unique_ptr<mb::UTable> table;
+  if (rows > 1 && mb::UTable::bytes_estimate(n, plan.count, sched) <= o.table_budget_bytes)
+    table = std::make_unique<mb::UTable>(bound, mb::StepWindow::of_plan(plan), sched);
+  Rows out;
+  out.rows = rows;
+  out.n = n;
+  out.eta.assign((std::size_t)(rows * n), 0.0);
+  out.rho.assign((std::size_t)(rows * n), cd(0.0, 0.0));
+  out.rhst.assign((std::size_t)rows, 0);
+  const long n_th0 = (long)grid.theta0.size();
+  mb::ProposedOptions popts;
+  popts.rhst_threshold = o.rhst_threshold;
+  auto solve_row = [&](long row) {
+    const double th1 = grid.theta1[(std::size_t)(row / n_th0)];
+    const double th0 = grid.theta0[(std::size_t)(row % n_th0)];
+    const mb::BeamGeometry beam(gamma, th0, th1);
+    const mb::GammaMatrix gm = mb::GammaMatrix::build(rods, beam);
+    mb::ComplexMatrix R_init;
+    if (bound.bulk_period())
+      R_init = mb::compute_bulk_reflection_proposed(bound, gm, o.dz, spec, popts, mb::BulkOptions{});
+    mb::SolveStats stats;
+    const mb::ComplexVector rho0 = mb::solve_proposed(bound, gm, plan, spec, popts, R_init, table.get(), &stats);
+    const mb::RealVector eta = mb::intensity(rho0, gm);
+    for (int i = 0; i < n; ++i) {
+      out.eta[(std::size_t)(row * n + i)] = eta(i);
+      out.rho[(std::size_t)(row * n + i)] = rho0(i);
+    }
+    out.rhst[(std::size_t)row] = stats.rhst_transforms;
+  };
+  const int threads = thread_count(o.threads, rows);
+  std::atomic<long> next{0};
+  std::vector<std::exception_ptr> errors((std::size_t)rows);
+  std::vector<std::thread> pool;
+  for (int t = 0; t < threads; ++t)
+    pool.emplace_back([&] {
+      for (;;) {
+        const long row = next.fetch_add(1, std::memory_order_relaxed);
+        if (row >= rows) return;
+        try {
+          solve_row(row);
+        } catch (...) {
+          errors[(std::size_t)row] = std::current_exception();
+        }
+      }
+    });
+  for (auto& th : pool) th.join();
+  for (long r = 0; r < rows; ++r)
+    if (errors[(std::size_t)r]) std::rethrow_exception(errors[(std::size_t)r]);
+  out.solve_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return out;
+}
+
+template <class T>
+py::array_t<T> arr2(const std::vector<T>& v, long r, long c) {
+  py::array_t<T> a({(py::ssize_t)r, (py::ssize_t)c});
+  if (!v.empty()) std::memcpy(a.mutable_data(), v.data(), v.size() * sizeof(T));
+  return a;
+}
+
+}  // namespace
+
+PYBIND11_MODULE(mb_ref, m) {
+  m.doc() =
+      "ORACLE (test infrastructure only): the reference hot path compiled verbatim from "
+      "/root/reference/proj/core/src against an Eigen-subset shim";
+
+  static py::exception<mb::Error> exc_error(m, "Error");
+  static py::exception<mb::ConfigError> exc_config(m, "ConfigError", exc_error.ptr());
+  static py::exception<mb::SolverError> exc_solver(m, "SolverError", exc_error.ptr());
+  static py::exception<mb::SingularMatrixError> exc_singular(m, "SingularMatrixError", exc_solver.ptr());
+  static py::exception<mb::BreakdownError> exc_breakdown(m, "BreakdownError", exc_solver.ptr());
+  static py::exception<mb::ConvergenceError> exc_conv(m, "ConvergenceError", exc_solver.ptr());
+  static py::exception<mb::DomainError> exc_domain(m, "DomainError", exc_solver.ptr());
+  static py::exception<mb::CompareError> exc_compare(m, "CompareError", exc_error.ptr());
+  py::register_exception_translator([](std::exception_ptr p) {
+    try {
+      if (p) std::rethrow_exception(p);
+    } catch (const mb::BreakdownError& e) {
+      py::object inst = py::reinterpret_borrow<py::object>(exc_breakdown.ptr())(e.what());
+      inst.attr("step") = e.step;
+      PyErr_SetObject(exc_breakdown.ptr(), inst.ptr());
+    } catch (const mb::SingularMatrixError& e) {
+      PyErr_SetString(exc_singular.ptr(), e.what());
+    } catch (const mb::ConvergenceError& e) {
+      PyErr_SetString(exc_conv.ptr(), e.what());
+    } catch (const mb::DomainError& e) {
+      PyErr_SetString(exc_domain.ptr(), e.what());
+    } catch (const mb::SolverError& e) {
+      PyErr_SetString(exc_solver.ptr(), e.what());
+    } catch (const mb::ConfigError& e) {
+      PyErr_SetString(exc_config.ptr(), e.what());
+    } catch (const mb::CompareError& e) {
+      PyErr_SetString(exc_compare.ptr(), e.what());
+    } catch (const mb::Error& e) {
+      PyErr_SetString(exc_error.ptr(), e.what());
+    }
+  });
+  m.attr("KIND") = "reference";
+
+  py::class_<mb::Lattice2D>(m, "Lattice2D")
+      .def(py::init([](std::pair<double, double> a1, std::pair<double, double> a2) {
+             mb::Lattice2D l;
+             l.a1 = mb::Vec2(a1.first, a1.second);
+             l.a2 = mb::Vec2(a2.first, a2.second);
+             return l;
+           }),
+           py::arg("a1"), py::arg("a2"));
+  py::class_<mb::RodSet>(m, "RodSet")
+      .def_static("build", &mb::RodSet::build, py::arg("lattice"), py::arg("cutoff"))
+      .def_static("build_first", &rods_first, py::arg("lattice"), py::arg("n"))
+      .def("size", &mb::RodSet::size)
+      .def("diff_count", &mb::RodSet::diff_count)
+      .def_property_readonly("k", [](const mb::RodSet& r) {
+        std::vector<double> v;
+        for (int i = 0; i < r.size(); ++i) v.push_back(r.k(i).x()), v.push_back(r.k(i).y());
+        return arr2(v, r.size(), 2);
+      })
+      .def_property_readonly("m", [](const mb::RodSet& r) {
+        std::vector<int> v;
+        for (int i = 0; i < r.size(); ++i) v.push_back(r.m(i).x()), v.push_back(r.m(i).y());
+        return arr2(v, r.size(), 2);
+      })
+      .def_property_readonly("diff_m", [](const mb::RodSet& r) {
+        std::vector<int> v;
+        for (int d = 0; d < r.diff_count(); ++d) v.push_back(r.diff_m(d).x()), v.push_back(r.diff_m(d).y());
+        return arr2(v, r.diff_count(), 2);
+      })
+      .def_property_readonly("diff_index", [](const mb::RodSet& r) {
+        std::vector<int> v;
+        for (int j = 0; j < r.size(); ++j)
+          for (int q = 0; q < r.size(); ++q) v.push_back(r.diff_index(j, q));
+        return arr2(v, r.size(), r.size());
+      });
+
+  m.def("gamma_matrix", [](const mb::RodSet& rods, double gamma, double th0, double th1) {
+    const mb::GammaMatrix g = mb::GammaMatrix::build(rods, mb::BeamGeometry(gamma, th0, th1));
+    std::vector<cd> d(g.diag().data(), g.diag().data() + g.size());
+    std::vector<cd> inv(g.inv_diag().data(), g.inv_diag().data() + g.size());
+    std::vector<double> g2(g.gamma2().data(), g.gamma2().data() + g.size());
+    std::vector<int> prop;
+    for (int i = 0; i < g.size(); ++i) prop.push_back(g.propagating(i));
+    return py::make_tuple(d, inv, g2, prop, g.sin_theta0());
+  });
+  m.def("node_heights", [](double z_bottom, double dz, const std::string& method) {
+    const mb::SlicingPlan plan = mb::SlicingPlan::with_target_dz(z_bottom, dz);
+    const mb::StepperSpec& spec = mb::StepperSpec::by_name(method);
+    const mb::NodeSchedule s = mb::schedule_for(spec);
+    const mb::StepWindow w = mb::StepWindow::of_plan(plan);
+    // the UTable slot order (stages.cpp:32-47)
+    std::vector<double> z;
+    const int k = s.nodes();
+    if (s.endpoint_pair()) {
+      for (long i = 0; i < w.count; ++i)
+        for (int q = 0; q < k - 1; ++q) z.push_back(mb::node_z(w, i, q, s));
+      z.push_back(mb::node_z(w, w.count - 1, k - 1, s));
+    } else {
+      collect_nodes(w, s, z);
+    }
+    return z;
+  });
+
+  py::class_<RefField>(m, "PotentialField")
+      .def_static("zero", [](double zb) { return RefField{mb::PotentialField::zero(zb), {}, zb, {}}; })
+      .def_static(
+          "gaussian_layers",
+          [](double zb, std::vector<std::tuple<double, double, double, double, double>> layers, py::object period) {
+            std::vector<mb::GaussianLayer> ls;
+            for (auto& t : layers)
+              ls.push_back(mb::GaussianLayer{std::get<0>(t), std::get<1>(t), std::get<2>(t), std::get<3>(t),
+                                             std::get<4>(t)});
+            std::optional<double> p;
+            if (!period.is_none()) p = period.cast<double>();
+            return RefField{mb::PotentialField::gaussian_layers(zb, std::move(ls), p), {}, zb, p};
+          },
+          py::arg("z_bottom"), py::arg("layers"), py::arg("bulk_period") = py::none())
+      .def_static(
+          "atoms",
+          [](double zb, py::array_t<double, py::array::forcecast> xyz, py::array_t<int, py::array::forcecast> species,
+             py::array_t<double, py::array::forcecast> B, py::array_t<double, py::array::forcecast> ff_a,
+             py::array_t<double, py::array::forcecast> ff_b, double cell_area, double gamma_L, double particle_sign,
+             double absorption, py::object period) {
+            mbo::AtomModel M;
+            auto x = xyz.unchecked<2>();
+            auto s = species.unchecked<1>();
+            auto bb = B.unchecked<1>();
+            for (py::ssize_t i = 0; i < xyz.shape(0); ++i)
+              M.atoms.push_back(mbo::AtomSite{x(i, 0), x(i, 1), x(i, 2), s(i), bb(i)});
+            auto fa = ff_a.unchecked<2>();
+            auto fb = ff_b.unchecked<2>();
+            for (py::ssize_t i = 0; i < ff_a.shape(0); ++i) {
+              mbo::Species sp;
+              for (int j = 0; j < 4; ++j) sp.a[j] = fa(i, j), sp.b[j] = fb(i, j);
+              M.species.push_back(sp);
+            }
+            M.cell_area = cell_area;
+            M.gamma_L = gamma_L;
+            M.particle_sign = particle_sign;
+            M.absorption = absorption;
+            std::optional<double> p;
+            if (!period.is_none()) p = period.cast<double>();
+            // validation as the restatement's atoms() (EXTENSION) plus the
+            // reference's own z_bottom / period checks via a zero field
+            (void)mb::PotentialField::gaussian_layers(zb, {}, p);
+            return RefField{std::nullopt, mbo::PotentialField::atoms(zb, std::move(M), p), zb, p};
+          },
+          py::arg("z_bottom"), py::arg("xyz"), py::arg("species"), py::arg("B"), py::arg("ff_a"), py::arg("ff_b"),
+          py::arg("cell_area"), py::arg("gamma_L"), py::arg("particle_sign"), py::arg("absorption"),
+          py::arg("bulk_period") = py::none())
+      .def_readonly("z_bottom", &RefField::z_bottom);
+
+  py::class_<mb::AngleGrid>(m, "AngleGrid")
+      .def_static("validated", &mb::AngleGrid::validated)
+      .def_readonly("theta0", &mb::AngleGrid::theta0)
+      .def_readonly("theta1", &mb::AngleGrid::theta1)
+      .def("rows", &mb::AngleGrid::rows);
+
+  py::class_<Opts>(m, "SweepOptions")
+      .def(py::init<>())
+      .def_readwrite("method", &Opts::method)
+      .def_readwrite("dz", &Opts::dz)
+      .def_readwrite("slices", &Opts::slices)
+      .def_readwrite("rhst_threshold", &Opts::rhst_threshold)
+      .def_readwrite("threads", &Opts::threads)
+      .def_readwrite("table_budget_bytes", &Opts::table_budget_bytes)
+      .def("set_splitting",
+           [](Opts& o, const std::string& name, const std::string& variant, std::vector<double> drift,
+              std::vector<double> kick) {
+             o.stepper = mb::StepperSpec::splitting(
+                 name, variant == "ABA" ? mb::SplitVariant::ABA : mb::SplitVariant::BAB, std::move(drift),
+                 std::move(kick));
+           });
+
+  py::class_<Rows>(m, "Rows")
+      .def_property_readonly("eta", [](const Rows& r) { return arr2(r.eta, r.rows, r.n); })
+      .def_property_readonly("rho", [](const Rows& r) { return arr2(r.rho, r.rows, r.n); })
+      .def_property_readonly("rhst", [](const Rows& r) {
+        py::array_t<long> a((py::ssize_t)r.rhst.size());
+        if (!r.rhst.empty()) std::memcpy(a.mutable_data(), r.rhst.data(), r.rhst.size() * sizeof(long));
+        return a;
+      })
+      .def_readonly("solve_seconds", &Rows::solve_seconds)
+      .def("rows", [](const Rows& r) { return r.rows; });
+
+  // rho + RHST counts per row (sweep.cpp:89-109 body); same surface as the
+  // restatement's rocking_curve so tests/harness.py can drive either.
+  m.def(
+      "solve_rows",
+      [](const RefField& f, const mb::RodSet& rods, double gamma, const mb::AngleGrid& grid, const Opts& o) {
+        return solve_rows(f, rods, gamma, grid, o);
+      },
+      py::call_guard<py::gil_scoped_release>());
+  // the reference's own sweep, unchanged (sweep.cpp:54-143): eta and timing
+  m.def(
+      "rocking_curve",
+      [](const RefField& f, const mb::RodSet& rods, double gamma, const mb::AngleGrid& grid, const Opts& o) {
+        const mb::StepperSpec& spec = spec_of(o);
+        const mb::SlicingPlan plan = plan_of(f, o);
+        const mb::PotentialField pf = realise(f, rods, plan, spec, o.dz, thread_count(o.threads, 1 << 20));
+        mb::SweepOptions so;
+        so.method = o.method;
+        so.dz = o.dz;
+        so.rhst_threshold = o.rhst_threshold;
+        so.threads = o.threads;
+        so.table_budget_bytes = o.table_budget_bytes;
+        const mb::RockingCurve c = mb::rocking_curve(pf, rods, gamma, grid, so);
+        std::vector<double> eta((std::size_t)(c.rows() * c.rod_count()));
+        for (long r = 0; r < c.rows(); ++r)
+          for (int i = 0; i < c.rod_count(); ++i) eta[(std::size_t)(r * c.rod_count() + i)] = c.eta(r, i);
+        return py::make_tuple(arr2(eta, c.rows(), c.rod_count()), c.solve_seconds);
+      },
+      py::call_guard<py::gil_scoped_release>());
+  m.def("curve_error", [](py::array_t<double, py::array::forcecast> cand, py::array_t<double, py::array::forcecast> ref,
+                          std::vector<double> theta0, std::vector<double> theta1) {
+    auto fill = [&](py::array_t<double, py::array::forcecast>& a) {
+      mb::RockingCurve c;
+      c.theta0 = theta0;
+      c.theta1 = theta1;
+      c.eta = mb::RealMatrix(a.shape(0), a.shape(1));
+      auto v = a.unchecked<2>();
+      for (py::ssize_t r = 0; r < a.shape(0); ++r)
+        for (py::ssize_t i = 0; i < a.shape(1); ++i) c.eta(r, i) = v(r, i);
+      return c;
+    };
+    return mb::curve_error(fill(cand), fill(ref));
+  });
+  m.def("gershgorin_cond", [](py::array_t<cd, py::array::forcecast> Q) {
+    auto v = Q.unchecked<2>();
+    mb::ComplexMatrix M(Q.shape(0), Q.shape(1));
+    for (py::ssize_t i = 0; i < Q.shape(0); ++i)
+      for (py::ssize_t j = 0; j < Q.shape(1); ++j) M(i, j) = v(i, j);
+    return mb::gershgorin_cond(M);
+  });
+}
