@@ -87,7 +87,9 @@ typedef struct {
   int kind;
   double z_bottom; /* A, < 0 */
   int has_bulk_period; /* bulk seed R_init per pair (compute_bulk_reflection_proposed,
-                          proposed.cpp:311-342); resident kernel (N <= 64) only */
+                          proposed.cpp:311-342): resident kernel (N <= 64) and cluster
+                          kernel (64 < N <= 256; rk4 only up to N = 128); other
+                          cases return MB_ERR_CONFIG */
   double bulk_period;
   /* MB_FIELD_GAUSSIAN_LAYERS: layers[nlayers][5] = z_center, amplitude,
    * sigma_xy, sigma_z, absorption */
@@ -203,6 +205,18 @@ int mb_plan_info(const mb_plan* plan, long* slots, int* ndiff, long* coef_bytes,
  * finite check, Gershgorin, RHST, surface solve, prologue) of the last
  * execute; all zero unless the library was built with MB_PROFILE */
 int mb_plan_profile(const mb_plan* plan, double* cycles12);
+/* EXTENSION (parity hooks; no reference counterpart): host copies of what
+ * mb_plan_create built, so tests can compare them with the reference.
+ *   node heights z[slots] in coefficient-table slot order (stages.cpp:25-47;
+ *     slab window then, with a bulk period, the mapped bulk window);
+ *   per pair Gamma[n][2], 1/Gamma[n][2], Gamma^2[n] and sin(theta0)
+ *     (GammaMatrix::build, geometry.cpp:30-57; any output may be null);
+ *   after an execute, the K1 coefficient table of one structure,
+ *     coef[slots][ndiff][2] (BoundPotential::eval_coeffs per node,
+ *     potential.cpp:169-199, plus the atom extension). cap counts doubles. */
+int mb_plan_node_heights(const mb_plan* plan, double* z, long cap);
+int mb_plan_gamma(const mb_plan* plan, long pair, double* gdiag, double* ginv, double* gamma2, double* sin_theta0);
+int mb_plan_coefficients(mb_plan* plan, int structure, double* coef, long cap);
 int mb_plan_destroy(mb_plan* plan);
 
 /* rocking_curve (sweep.hpp:37-38, sweep.cpp:54-143), stepper methods:

@@ -22,11 +22,12 @@
 //     (potential.cpp:189-197: t = 0 or 1 there), so the reference propagates
 //     the atom potential itself. Bulk-period heights are added after the
 //     reference's map_z (potential.cpp:152-167, restated bit for bit below).
-//   * solve_rows(...): sweep.cpp:89-109's per-row body (BeamGeometry,
+//   * rocking_curve(...): sweep.cpp:89-109's per-row body (BeamGeometry,
 //     GammaMatrix, bulk seed, solve_proposed with the shared UTable) with
 //     SolveStats and rho kept, over the same atomic-counter thread pool
-//     (sweep.cpp:111-138). rocking_curve(...) calls the reference's own
-//     manybeam::rocking_curve unchanged (eta only).
+//     (sweep.cpp:111-138), returning eta, rho and the RHST counts (the
+//     restatement's surface). reference_sweep(...) calls the reference's own
+//     manybeam::rocking_curve unchanged (eta and solve_seconds).
 #include <pybind11/numpy.h>
 #include <pybind11/pybind11.h>
 #include <pybind11/stl.h>
@@ -493,31 +494,39 @@ PYBIND11_MODULE(mb_ref, m) {
   // rho + RHST counts per row (sweep.cpp:89-109 body); same surface as the
   // restatement's rocking_curve so tests/harness.py can drive either.
   m.def(
-      "solve_rows",
+      "rocking_curve",
       [](const RefField& f, const mb::RodSet& rods, double gamma, const mb::AngleGrid& grid, const Opts& o) {
         return solve_rows(f, rods, gamma, grid, o);
       },
       py::call_guard<py::gil_scoped_release>());
-  // the reference's own sweep, unchanged (sweep.cpp:54-143): eta and timing
-  m.def(
-      "rocking_curve",
-      [](const RefField& f, const mb::RodSet& rods, double gamma, const mb::AngleGrid& grid, const Opts& o) {
-        const mb::StepperSpec& spec = spec_of(o);
-        const mb::SlicingPlan plan = plan_of(f, o);
-        const mb::PotentialField pf = realise(f, rods, plan, spec, o.dz, thread_count(o.threads, 1 << 20));
-        mb::SweepOptions so;
-        so.method = o.method;
-        so.dz = o.dz;
-        so.rhst_threshold = o.rhst_threshold;
-        so.threads = o.threads;
-        so.table_budget_bytes = o.table_budget_bytes;
-        const mb::RockingCurve c = mb::rocking_curve(pf, rods, gamma, grid, so);
-        std::vector<double> eta((std::size_t)(c.rows() * c.rod_count()));
-        for (long r = 0; r < c.rows(); ++r)
-          for (int i = 0; i < c.rod_count(); ++i) eta[(std::size_t)(r * c.rod_count() + i)] = c.eta(r, i);
-        return py::make_tuple(arr2(eta, c.rows(), c.rod_count()), c.solve_seconds);
-      },
-      py::call_guard<py::gil_scoped_release>());
+  // the reference's own sweep, unchanged (sweep.cpp:54-143): (eta, solve_seconds)
+  m.def("reference_sweep", [](const RefField& f, const mb::RodSet& rods, double gamma, const mb::AngleGrid& grid,
+                              const Opts& o) {
+    std::vector<double> eta;
+    long rows = 0;
+    int nr = 0;
+    double secs = 0.0;
+    {
+      py::gil_scoped_release nogil;
+      const mb::StepperSpec& spec = spec_of(o);
+      const mb::SlicingPlan plan = plan_of(f, o);
+      const mb::PotentialField pf = realise(f, rods, plan, spec, o.dz, thread_count(o.threads, 1 << 20));
+      mb::SweepOptions so;
+      so.method = o.method;
+      so.dz = o.dz;
+      so.rhst_threshold = o.rhst_threshold;
+      so.threads = o.threads;
+      so.table_budget_bytes = o.table_budget_bytes;
+      const mb::RockingCurve c = mb::rocking_curve(pf, rods, gamma, grid, so);
+      rows = c.rows();
+      nr = c.rod_count();
+      eta.resize((std::size_t)(rows * nr));
+      for (long r = 0; r < rows; ++r)
+        for (int i = 0; i < nr; ++i) eta[(std::size_t)(r * nr + i)] = c.eta(r, i);
+      secs = c.solve_seconds;
+    }
+    return py::make_tuple(arr2(eta, rows, nr), secs);
+  });
   m.def("curve_error", [](py::array_t<double, py::array::forcecast> cand, py::array_t<double, py::array::forcecast> ref,
                           std::vector<double> theta0, std::vector<double> theta1) {
     auto fill = [&](py::array_t<double, py::array::forcecast>& a) {

@@ -162,6 +162,9 @@ def lib():
                                    C.POINTER(C.c_int), C.POINTER(C.c_long)]
         L.mb_plan_destroy.argtypes = [C.c_void_p]
         L.mb_plan_profile.argtypes = [C.c_void_p, C.c_void_p]
+        L.mb_plan_node_heights.argtypes = [C.c_void_p, C.c_void_p, C.c_long]
+        L.mb_plan_gamma.argtypes = [C.c_void_p, C.c_long, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.mb_plan_coefficients.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_long]
         L.mb_rocking_curve.argtypes = [C.c_void_p, C.POINTER(_Field), C.POINTER(_Rods), C.c_double, C.c_void_p,
                                        C.c_int, C.c_void_p, C.c_int, C.POINTER(_Stepper), C.POINTER(_Options),
                                        C.c_void_p, C.c_void_p, C.c_void_p]
@@ -542,6 +545,26 @@ class Plan:
         v = np.zeros(12)
         _check(lib().mb_plan_profile(self._h, _ptr(v)))
         return dict(zip(self.PHASES, v.tolist()))
+
+    # parity hooks (EXTENSION): what plan creation / K1 produced
+    def node_heights(self):
+        z = np.zeros(self.info()["slots"])
+        _check(lib().mb_plan_node_heights(self._h, _ptr(z), len(z)))
+        return z
+
+    def gamma(self, pair):
+        gd = np.zeros(self.n, np.complex128)
+        gi = np.zeros(self.n, np.complex128)
+        g2 = np.zeros(self.n)
+        s0 = C.c_double()
+        _check(lib().mb_plan_gamma(self._h, int(pair), _ptr(gd), _ptr(gi), _ptr(g2), C.byref(s0)))
+        return gd, gi, g2, s0.value
+
+    def coefficients(self, structure=0):
+        inf = self.info()
+        c = np.zeros((inf["slots"], inf["ndiff"]), np.complex128)
+        _check(lib().mb_plan_coefficients(self._h, int(structure), _ptr(c), 2 * c.size))
+        return c
 
     def close(self):
         if self._h:

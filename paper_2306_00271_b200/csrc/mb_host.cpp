@@ -212,7 +212,9 @@ void validate_stepper(const mb_stepper& s) {
   }
   if (std::abs(sa - 1.0) > 1e-13 || std::abs(sb - 1.0) > 1e-13)
     fail(MB_ERR_CONFIG, "stepper: drift and kick coefficients must each sum to 1");
-  if (nk > mbx::kMaxOcc) fail(MB_ERR_CONFIG, "stepper: too many stages for the device kernel");
+  // occ_kick / occ_drift hold one entry per kick and per drift (ABA has one
+  // more drift than kicks)
+  if (std::max(nk, nd) > mbx::kMaxOcc) fail(MB_ERR_CONFIG, "stepper: too many stages for the device kernel");
 }
 
 // stages.cpp:12-23
@@ -428,6 +430,9 @@ struct mb_plan {
   long h2d_bytes = 0;
   bool executed = false;
   std::vector<double2> host_coef;  // tabulated / zero fields: precomputed table
+  // host copies kept for the parity hooks (mb_plan_node_heights / mb_plan_gamma)
+  std::vector<double> zslot, g2, s0;
+  std::vector<double2> gd, gi;
 };
 
 namespace {
@@ -626,6 +631,11 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
     pl->npairs = npairs;
     pl->nslots = nslots;
     pl->S = nfields;
+    pl->zslot = zslot;
+    pl->g2 = g2;
+    pl->s0 = s0;
+    pl->gd = gd;
+    pl->gi = gi;
     cudaStream_t st = ctx->stream;
 
     // ---- coefficient table: K1 terms (atoms / gaussian layers) or host table
@@ -1113,6 +1123,43 @@ int mb_plan_profile(const mb_plan* plan, double* cycles) {
     unsigned long long v[12];
     cuda_check(cudaMemcpy(v, plan->prop.prof, sizeof v, cudaMemcpyDeviceToHost), "D2H profile");
     for (int q = 0; q < 12; ++q) cycles[q] = (double)v[q] / (double)plan->npairs;
+  });
+}
+
+int mb_plan_node_heights(const mb_plan* plan, double* z, long cap) {
+  return guarded([&] {
+    if (!plan || !z) fail(MB_ERR_ARG, "null argument");
+    if (cap < (long)plan->zslot.size()) fail(MB_ERR_ARG, "mb_plan_node_heights: capacity too small");
+    std::memcpy(z, plan->zslot.data(), plan->zslot.size() * sizeof(double));
+  });
+}
+
+int mb_plan_gamma(const mb_plan* plan, long pair, double* gdiag, double* ginv, double* gamma2, double* sin_theta0) {
+  return guarded([&] {
+    if (!plan) fail(MB_ERR_ARG, "null plan");
+    if (pair < 0 || pair >= plan->npairs) fail(MB_ERR_ARG, "mb_plan_gamma: pair index out of range");
+    const std::size_t o = (std::size_t)pair * plan->n;
+    for (int i = 0; i < plan->n; ++i) {
+      if (gdiag) gdiag[2 * i] = plan->gd[o + i].x, gdiag[2 * i + 1] = plan->gd[o + i].y;
+      if (ginv) ginv[2 * i] = plan->gi[o + i].x, ginv[2 * i + 1] = plan->gi[o + i].y;
+      if (gamma2) gamma2[i] = plan->g2[o + i];
+    }
+    if (sin_theta0) *sin_theta0 = plan->s0[(std::size_t)pair];
+  });
+}
+
+int mb_plan_coefficients(mb_plan* plan, int structure, double* coef, long cap) {
+  return guarded([&] {
+    if (!plan || !coef) fail(MB_ERR_ARG, "null argument");
+    if (structure < 0 || structure >= plan->S) fail(MB_ERR_ARG, "mb_plan_coefficients: structure out of range");
+    if (!plan->executed) fail(MB_ERR_ARG, "plan has not been executed");
+    const std::size_t cnt = (std::size_t)plan->nslots * plan->ndiff;
+    if (cap < (long)(2 * cnt)) fail(MB_ERR_ARG, "mb_plan_coefficients: capacity too small");
+    std::lock_guard<std::mutex> lk(plan->ctx->mu);
+    cuda_check(cudaMemcpyAsync(coef, plan->prop.coef + (std::size_t)structure * cnt, cnt * sizeof(double2),
+                               cudaMemcpyDeviceToHost, plan->ctx->stream),
+               "D2H coefficient table");
+    cuda_check(cudaStreamSynchronize(plan->ctx->stream), "D2H coefficient table");
   });
 }
 

@@ -1,9 +1,11 @@
-"""Generates the committed golden fixtures from the oracle (CPU restatement of
-the reference hot path; the reference ships no golden vectors
-and cannot be built here, so the oracle, pinned by the reference's own
-known-answer tests in tests/test_oracle_*.py, is the reference of record).
+"""Generates the committed golden fixtures from the REFERENCE ITSELF: the
+reference's hot-path sources compiled verbatim against the Eigen-subset shim
+(oracle/_ref/mb_ref*.so, `make -C oracle ref`; SURVEY.md §8c option A). The
+reference ships no golden vectors of its own, and its atom
+potential enters as a Tabulated field on the exact node heights (see
+oracle/ref/mb_ref_py.cpp).
 
-    python tests/golden/make_golden.py
+    python tests/golden/make_golden.py [case ...]
 
 Each fixture stores the workload parameters (so it is self-describing), the
 intensities eta[pairs][n], the reflection amplitudes rho, and the RHST counts.
@@ -17,9 +19,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
-sys.path.insert(0, os.path.join(ROOT, "oracle", "_build"))
+sys.path.insert(0, os.path.join(ROOT, "oracle", "_ref"))
 
-import mb_oracle  # noqa: E402
+import mb_ref  # noqa: E402
 
 import harness as H  # noqa: E402
 from paper_2306_00271_b200 import configs  # noqa: E402
@@ -51,10 +53,10 @@ CASES = {
 
 def make(name):
     w = CASES[name]()
-    eta, rho, rh = H.run_oracle(mb_oracle, w, threads=0)
+    eta, rho, rh = H.run_oracle(mb_ref, w, threads=0)
     np.savez_compressed(os.path.join(HERE, f"{name}.npz"), eta=eta, rho=rho, rhst=rh, n_rods=w.n_rods,
                         slices=w.slices, method=w.method, theta0=np.array(w.theta0), z_bottom=w.z_bottom,
-                        structures=len(w.structures))
+                        structures=len(w.structures), generator="oracle/_ref (reference sources, verbatim)")
     print(name, eta.shape, "rhst", rh.tolist()[:6])
 
 

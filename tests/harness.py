@@ -1,6 +1,8 @@
-"""Shared parity harness: runs one workload through the oracle (CPU
-restatement, test infrastructure) and through the device path
-(libmanybeam_b200.so via the Python mirror) on identical seeded inputs."""
+"""Shared parity harness: runs one workload through a CPU checker (the
+reference compiled from its own sources, oracle/_ref `mb_ref`, or the
+restatement oracle/_build `mb_oracle`; both test infrastructure, same Python
+surface) and through the device path (libmanybeam_b200.so via the Python
+mirror) on identical seeded inputs."""
 import math
 
 import numpy as np
@@ -55,11 +57,10 @@ def curve_err(eta, ref):
     return 0.0 if num == 0 else (math.inf if den == 0 else num / den)
 
 
-def entry_rel_err(eta, ref, floor=1e-10):
-    """Per-entry relative error on entries >= floor * max eta. Entries below
-    the floor are checked absolutely by entry_abs_err: at 1e-12 * max eta a
-    1e-9 relative bound would be ~1e-21 absolute, under the FP64 noise that
-    one-ulp differences in a pivot reciprocal leave after ~10^2 RHST solves."""
+def entry_rel_err(eta, ref, floor=1e-12):
+    """Per-entry relative error on entries >= floor * max eta (SURVEY.md §8d:
+    1e-9 relative on entries above 1e-12 * max eta). Entries below the floor
+    are checked absolutely by entry_abs_err."""
     mask = np.abs(ref) >= floor * np.abs(ref).max()
     return float((np.abs(eta - ref)[mask] / np.abs(ref)[mask]).max())
 

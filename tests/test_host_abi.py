@@ -52,6 +52,25 @@ def test_rods_match_oracle_bitwise(oracle, cell, n):
     assert np.array_equal(r.diff_index, o.diff_index)
 
 
+@pytest.mark.parametrize("cell,n", [(("hex", 3.84), 13), (("hex", 3.84), 63), (("rect", 7.68, 3.84), 61),
+                                    (("hex", 19.2), 199), (("hex", 3.84), 255)])
+def test_rods_match_reference_bitwise(ref, cell, n):
+    """The product's host rod tables against the reference's own RodSet::build
+    (oracle/_ref; first-N by truncating the reference's total order)."""
+    lat = mb.Lattice2D.hexagonal(cell[1]) if cell[0] == "hex" else mb.Lattice2D.rectangular(cell[1], cell[2])
+    r = mb.RodSet.build_first(lat, n)
+    o = ref.RodSet.build_first(ref.Lattice2D(lat.a1, lat.a2), n)
+    assert np.array_equal(r.k, o.k) and np.array_equal(r.m, o.m)
+    assert np.array_equal(r.diff_m, o.diff_m) and np.array_equal(r.diff_index, o.diff_index)
+
+
+def test_rods_cutoff_build_matches_reference(ref):
+    lat = mb.Lattice2D((2.0, 0.0), (0.0, 2.6))
+    r = mb.RodSet.build(lat, 5.0)
+    o = ref.RodSet.build(ref.Lattice2D(lat.a1, lat.a2), 5.0)
+    assert r.size() == 11 and np.array_equal(r.k, o.k) and np.array_equal(r.diff_index, o.diff_index)
+
+
 def test_rods_cutoff_build_matches_oracle(oracle):
     lat = mb.Lattice2D((2.0, 0.0), (0.0, 2.6))
     r = mb.RodSet.build(lat, 5.0)
