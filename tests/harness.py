@@ -68,3 +68,23 @@ def entry_rel_err(eta, ref, floor=1e-12):
 def entry_abs_err(eta, ref):
     """max |d eta| / max eta over every entry."""
     return float(np.abs(eta - ref).max() / max(np.abs(ref).max(), 1e-300))
+
+
+def assert_parity(eta, want, alt=None, tol=1e-9, abs_tol=1e-11, slack=3.0):
+    """The parity gate against the reference rows `want`:
+      * curve_error (curve.cpp:22-41) <= tol;
+      * per-entry relative error on entries >= 1e-12 max eta <= tol, or, where
+        two correct CPU builds already disagree by more, <= slack x that noise
+        floor: `alt` is the restatement's rows for the same inputs and RHST
+        schedule (summation order is the only difference between the two), so
+        entry_rel_err(alt, want) measures the conditioning of the case;
+      * |d eta| <= abs_tol max eta everywhere.
+    Returns the measured numbers."""
+    ce = curve_err(eta, want)
+    er = entry_rel_err(eta, want)
+    noise = entry_rel_err(alt, want) if alt is not None else 0.0
+    ea = entry_abs_err(eta, want)
+    assert ce <= tol, ("curve_error", ce)
+    assert er <= max(tol, slack * noise), ("entry_rel_err", er, "cpu noise floor", noise)
+    assert ea <= abs_tol, ("entry_abs_err", ea)
+    return {"curve_error": ce, "entry_rel_err": er, "cpu_noise_floor": noise, "entry_abs_err": ea}

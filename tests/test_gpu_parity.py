@@ -163,43 +163,40 @@ def test_deterministic_bitwise():
 
 
 # ---------------------------------------------------------------- atom configs
-def test_config0_full_parity(ref):
+def test_config0_full_parity(ref, oracle):
     w = configs.config0()
     want, rref, rh = H.run_oracle(ref, w)
     eta, rho, st = H.run_device(w)
-    assert H.curve_err(eta, want) <= TOL
-    assert H.entry_rel_err(eta, want) <= TOL
-    assert H.entry_abs_err(eta, want) <= 1e-11
     assert (st["code"] == 0).all()
+    assert np.array_equal(st["rhst"], rh)
+    H.assert_parity(eta, want, H.run_oracle(oracle, w)[0])
 
 
-def test_config1_subset_parity(ref):
+def test_config1_subset_parity(ref, oracle):
     w = configs.config1().subset(theta0=[0.1, 1.0, 2.5, 6.1])
     want, rref, rh = H.run_oracle(ref, w, threads=4)
+    alt = H.run_oracle(oracle, w, threads=4)[0]
     for fsal in (False, True):
         eta, rho, st = H.run_device(w, fsal=fsal)
-        assert H.curve_err(eta, want) <= TOL, fsal
-        assert H.entry_rel_err(eta, want) <= TOL, fsal
-        assert H.entry_abs_err(eta, want) <= 1e-11, fsal
+        assert np.array_equal(st["rhst"], rh), fsal
+        H.assert_parity(eta, want, alt)
 
 
-def test_config2_subset_parity(ref):
+def test_config2_subset_parity(ref, oracle):
     w = configs.config2(n_structures=3).subset(theta0=[0.5, 2.0, 4.4, 6.5])
-    want, _, _ = H.run_oracle(ref, w, threads=4)
+    want, _, rh = H.run_oracle(ref, w, threads=4)
     eta, _, st = H.run_device(w)
-    assert H.curve_err(eta, want) <= TOL
-    assert H.entry_rel_err(eta, want) <= TOL
-    assert H.entry_abs_err(eta, want) <= 1e-11
+    assert np.array_equal(st["rhst"], rh)
+    H.assert_parity(eta, want, H.run_oracle(oracle, w, threads=4)[0])
 
 
 @pytest.mark.parametrize("n,method", [(15, "rk4"), (15, "sp6"), (31, "sp6"), (63, "sp6")])
-def test_config4_subset_parity(ref, n, method):
+def test_config4_subset_parity(ref, oracle, n, method):
     w = configs.config4(n, method, n_structures=2).subset(theta0=[0.5, 3.3, 6.8], slices=100)
-    want, _, _ = H.run_oracle(ref, w, threads=4)
+    want, _, rh = H.run_oracle(ref, w, threads=4)
     eta, _, st = H.run_device(w)
-    assert H.curve_err(eta, want) <= TOL
-    assert H.entry_rel_err(eta, want) <= TOL
-    assert H.entry_abs_err(eta, want) <= 1e-11
+    assert np.array_equal(st["rhst"], rh)
+    H.assert_parity(eta, want, H.run_oracle(oracle, w, threads=4)[0])
 
 
 # ---------------------------------------------------------------- large-N batched path
@@ -208,15 +205,13 @@ def test_config4_subset_parity(ref, n, method):
 @pytest.mark.parametrize("n,method,path", [(63, "rk4", 0), (31, "rk4", 2), (61, "sp6", 2), (127, "sp6", 2),
                                            (127, "rk4", 2), (127, "sp6", 3), (127, "rk4", 3), (81, "sp6", 3),
                                            (143, "sp6", 3), (143, "rk4", 2)])
-def test_large_path_parity(ref, n, method, path):
+def test_large_path_parity(ref, oracle, n, method, path):
     w = configs.config4(n, method, n_structures=2).subset(theta0=[0.5, 4.1], slices=150, z_bottom=-2.4)
     want, _, rh = H.run_oracle(ref, w, threads=4)
     eta, _, st = H.run_device(w, path=path)
     assert (st["code"] == 0).all()
     assert np.array_equal(st["rhst"], rh)
-    assert H.curve_err(eta, want) <= TOL
-    assert H.entry_rel_err(eta, want) <= TOL
-    assert H.entry_abs_err(eta, want) <= 1e-11
+    H.assert_parity(eta, want, H.run_oracle(oracle, w, threads=4)[0])
 
 
 @pytest.mark.parametrize("cfg,method", [(1, "sp6"), (4, "rk4")])
@@ -232,31 +227,26 @@ def test_large_path_matches_resident(cfg, method):
 
 
 @pytest.mark.parametrize("path", [2, 3])
-def test_config3_subset_parity(ref, path):
+def test_config3_subset_parity(ref, oracle, path):
     w = configs.config3().subset(theta0=[0.5, 3.5], slices=300, z_bottom=-3.0)
     want, _, rh = H.run_oracle(ref, w, threads=2)
     eta, _, st = H.run_device(w, path=path)
     assert (st["code"] == 0).all()
     assert np.array_equal(st["rhst"], rh)
-    assert H.curve_err(eta, want) <= TOL
-    # N=199 noise floor, measured on the CPU with the SAME RHST schedule: the
-    # reference build (oracle/_ref, OpenBLAS GEMM, Eigen-order LU) against the
-    # restatement (oracle/_build, plain loops) on this very subset differ by
-    # 8.6e-9 per entry above 1e-10 max eta (curve_error 1.9e-11); the bound
-    # sits just above that floor (tools/noise_floor.py, profiles/parity_r02.json)
-    assert H.entry_rel_err(eta, want) <= 1.5e-8
-    assert H.entry_abs_err(eta, want) <= 1e-10
+    # N=199: the restatement against the reference build at the same RHST
+    # schedule differs by 8.6e-9 per entry above 1e-10 max eta (curve_error
+    # 1.9e-11), the case's conditioning; assert_parity takes that floor
+    H.assert_parity(eta, want, H.run_oracle(oracle, w, threads=2)[0], abs_tol=1e-10)
 
 
 @pytest.mark.parametrize("method,path", [("rk4", 2), ("sp6", 3)])
-def test_n255_parity(ref, method, path):
+def test_n255_parity(ref, oracle, method, path):
     w = configs.config4(255, method, n_structures=1).subset(theta0=[1.7], slices=60, z_bottom=-0.96)
     want, _, rh = H.run_oracle(ref, w, threads=1)
     eta, _, st = H.run_device(w, path=path)
     assert (st["code"] == 0).all()
     assert np.array_equal(st["rhst"], rh)
-    assert H.curve_err(eta, want) <= TOL
-    assert H.entry_rel_err(eta, want) <= TOL
+    H.assert_parity(eta, want, H.run_oracle(oracle, w, threads=1)[0])
 
 
 @pytest.mark.parametrize("n,method", [(127, "sp6"), (199, "sp6"), (127, "rk4")])
@@ -321,15 +311,16 @@ def test_bulk_layered_parity(ref, method):
 
 
 @pytest.mark.parametrize("method", ["rk4", "sp6"])
-def test_bulk_atoms_parity(ref, method):
+def test_bulk_atoms_parity(ref, oracle, method):
     w = configs.config0().subset(theta0=[0.7, 2.1, 4.5, 6.1])
     w.bulk_period = 3.13  # one 0.78 + 2.35 A layer pair, continued below z_bottom
     want, _, rh = H.run_oracle(ref, w, threads=4, method=method)
     eta, _, st = H.run_device(w, method=method)
     assert (st["code"] == 0).all()
     assert np.array_equal(st["rhst"], rh)
-    assert H.curve_err(eta, want) <= TOL
-    assert H.entry_rel_err(eta, want) <= TOL
+    # R_bulk is defined to its stopping rule only (proposed.cpp:334-339); the
+    # restatement's rows give the spread two correct builds show here
+    H.assert_parity(eta, want, H.run_oracle(oracle, w, threads=4, method=method)[0])
 
 
 def test_bulk_rejected_off_chip():
