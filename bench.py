@@ -77,7 +77,8 @@ class Clocks:
          "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, device):
-        self.device, self.proc, self.path = device, None, f"/tmp/mb_clocks_{os.getpid()}_{device}.csv"
+        self.device, self.proc = device, None
+        self.path = f"/tmp/mb_clocks_{os.getpid()}_{str(device).replace(',', '_')}.csv"
 
     def start(self):
         try:
@@ -184,7 +185,7 @@ def run_leg(mb, configs, torch, cfg, w, args, ctx, rank, world, dist, local_rank
         if plan:
             plan.execute()
     barrier()
-    clocks = Clocks(local_rank)
+    clocks = Clocks(",".join(str(d) for d in ctx.devices))
     clocks.start()
     tot = pot = prop = 0.0
     launches = 0
@@ -307,8 +308,8 @@ def cpu_baseline(w, eta_dev=None):
     """The reference (oracle/_ref) on the bounded sample, timed by its own
     sweep timer (sweep.cpp:56,140-141) with threads = host cores; plus the
     device rows of the same points compared with it."""
-    import harness as H
     mb_ref = _ref_module()
+    import harness as H
     cores = os.cpu_count() or 1
     sub, idx = ref_sample(w, cores)
     rods = mb_ref.RodSet.build_first(mb_ref.Lattice2D(sub.a1, sub.a2), sub.n_rods)
@@ -412,18 +413,25 @@ def main():
     ap.add_argument("--no-fsal", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--launcher", default="context", choices=["context", "torchrun"],
+                    help="--gpus N without torchrun: one process over a multi-device context, or relaunch")
     args = ap.parse_args()
     rank, local_rank, world = dist_env()
     if args.impl == "reference":
         return run_reference(args)
-    if world == 1 and args.gpus > 1:
+    if world == 1 and args.gpus > 1 and args.launcher == "torchrun":
         return relaunch(args)
     if world != args.gpus and "WORLD_SIZE" in os.environ and args.gpus != 1:
         raise SystemExit(f"--gpus {args.gpus} disagrees with WORLD_SIZE={world}")
+    # --gpus N in one process: the library's multi-device context
+    # (mb_context_create_multi: one host thread per GPU, fixed pair map, rows
+    # gathered in order); under torchrun each rank drives its own GPU
+    ndev = args.gpus if world == 1 else 1
 
     import torch
-    if torch.cuda.device_count() <= local_rank:
-        raise SystemExit(f"rank {rank}: no CUDA device {local_rank} visible (no CPU fallback)")
+    if torch.cuda.device_count() < max(ndev, local_rank + 1):
+        raise SystemExit(f"rank {rank}: needs {max(ndev, local_rank + 1)} CUDA device(s), "
+                         f"{torch.cuda.device_count()} visible (no CPU fallback)")
     torch.cuda.set_device(local_rank)
     dist = None
     if world > 1:
@@ -432,7 +440,7 @@ def main():
     import paper_2306_00271_b200 as mb
     from paper_2306_00271_b200 import configs
 
-    ctx = mb.Context(local_rank)
+    ctx = mb.Context(devices=list(range(ndev))) if ndev > 1 else mb.Context(local_rank)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > 126 MB L2
     w = workload(args.config, args)
     if args.method:
@@ -451,12 +459,21 @@ def main():
 
     if rank == 0:
         cb, parity = None, None
-        if not args.no_cpu_baseline and world == 1:
+        if not args.no_cpu_baseline and world == 1 and ndev == 1:
             rows, eta, *_ = state
             cb, parity, _ = cpu_baseline(w, eta)
         sharded = world > 1
+        if ndev > 1:
+            par = (f"one process, mb_context_create_multi over {ndev} GPUs (" +
+                   ("angles round-robin" if len(w.structures) == 1 else "contiguous structure blocks") +
+                   "), no collective")
+        elif sharded:
+            par = (("angles round-robin" if len(w.structures) == 1 else "contiguous structure blocks") +
+                   f" over {world} rank(s), no collective")
+        else:
+            par = "1 GPU"
         line = {
-            "metric": METRIC, "value": head["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": METRIC, "value": head["value"], "unit": UNIT, "n_gpus": world * ndev, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": w.name, "points": w.points(), "n_rods": w.n_rods, "method": head["method"],
@@ -464,9 +481,7 @@ def main():
                        "rhst_threshold": 1000.0, "residual_check": True,
                        "l2": "flushed between steps (512 MiB write); coefficient table "
                              f"{head['coef_table_mib']:.1f} MiB",
-                       "parallelism": (("angles round-robin" if len(w.structures) == 1 else
-                                        "contiguous structure blocks") + f" over {world} rank(s), no collective")
-                       if sharded else "1 GPU"},
+                       "parallelism": par},
             "roofline": head["roofline"], "potential_roofline": head.get("potential_roofline"),
             "cpu_baseline": cb, "parity": parity, "e2e": e2e, "gpu_launches": head["gpu_launches"],
             "kernel_ms": head["kernel_ms"], "rhst_per_point": head["rhst_per_point"],

@@ -176,6 +176,19 @@ typedef struct {
 /* One context per device; owns streams and a grow-only device arena reused
  * across calls. Thread-safe per context (calls serialize on an internal lock). */
 int mb_context_create(int device, mb_context** out);
+/* Several devices behind one context (the reference's
+ * rocking_curve spreads its rows over the machine, sweep.cpp:111-138). A plan
+ * made on it splits its pairs over the devices with a fixed map: contiguous
+ * structure blocks balanced by pair count when it has several fields (each
+ * structure's coefficient table is built on one device only), pairs
+ * round-robin when it has one. mb_plan_execute runs every device's share on
+ * its own host thread; mb_plan_results gathers the rows into the caller's
+ * arrays in pair order, so the output does not depend on the device count.
+ * A device may be listed twice (two shards on one GPU, separate streams).
+ * Timing reports the slowest device; launches are summed. */
+int mb_context_create_multi(const int* devices, int ndevices, mb_context** out);
+/* devices behind a context (1 for mb_context_create) */
+int mb_context_device_count(const mb_context* ctx);
 int mb_context_destroy(mb_context* ctx);
 const char* mb_last_error(void);
 /* 1 when the library was built for sm_100a and a matching device is present */

@@ -240,10 +240,12 @@ struct Rows {
 // sweep.cpp:54-143 with the per-row body of :89-109, keeping rho and SolveStats.
 Rows solve_rows(const RefField& field, const mb::RodSet& rods, double gamma, const mb::AngleGrid& grid,
                 const Opts& o) {
-  const auto t0 = std::chrono::steady_clock::now();
   const mb::StepperSpec& spec = spec_of(o);
   const mb::SlicingPlan plan = plan_of(field, o);
   const mb::PotentialField pf = realise(field, rods, plan, spec, o.dz, thread_count(o.threads, 1 << 20));
+  // timed like sweep.cpp:56,140-141 (BoundPotential, UTable and the row pool);
+  // the atom-model tabulation above is the extension's input preparation
+  const auto t0 = std::chrono::steady_clock::now();
   const mb::BoundPotential bound(pf, rods);
   const long rows = grid.rows();
   const int n = rods.size();

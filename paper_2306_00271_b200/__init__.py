@@ -150,6 +150,8 @@ def lib():
         L.mb_stepper_by_name.argtypes = [C.c_char_p, C.POINTER(_Stepper)]
         L.mb_context_create.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
         L.mb_context_destroy.argtypes = [C.c_void_p]
+        L.mb_context_create_multi.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]
+        L.mb_context_device_count.argtypes = [C.c_void_p]
         L.mb_device_ok.argtypes = [C.c_int]
         L.mb_plan_create.argtypes = [C.c_void_p, C.POINTER(_Rods), C.POINTER(_Field), C.c_int, C.c_double,
                                      C.POINTER(_Pair), C.c_long, C.POINTER(_Stepper), C.POINTER(_Options),
@@ -465,12 +467,19 @@ class RockingCurve:
 
 
 class Context:
-    """One device context (streams + pooled device memory)."""
+    """A device context (streams + pooled device memory). With `devices`
+    (a list, repeats allowed) one context drives several GPUs: plans split
+    their pairs over them (mb_context_create_multi)."""
 
-    def __init__(self, device=0):
+    def __init__(self, device=0, devices=None):
         self._h = C.c_void_p()
-        _check(lib().mb_context_create(int(device), C.byref(self._h)))
-        self.device = device
+        if devices is not None:
+            arr = (C.c_int * len(devices))(*[int(d) for d in devices])
+            _check(lib().mb_context_create_multi(arr, len(devices), C.byref(self._h)))
+            self.device, self.devices = int(devices[0]), list(devices)
+        else:
+            _check(lib().mb_context_create(int(device), C.byref(self._h)))
+            self.device, self.devices = device, [device]
 
     def close(self):
         if self._h:

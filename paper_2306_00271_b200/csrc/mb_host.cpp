@@ -15,6 +15,8 @@
 #include <limits>
 #include <map>
 #include <mutex>
+#include <thread>
+#include <exception>
 #include <numeric>
 #include <stdexcept>
 #include <string>
@@ -409,6 +411,9 @@ struct mb_context {
   int device = 0;
   cudaStream_t stream = nullptr;
   std::mutex mu;
+  // multi-device context (mb_context_create_multi): one single-device
+  // sub-context per listed device; empty for a plain context
+  std::vector<mb_context*> subs;
 };
 
 struct mb_plan {
@@ -433,6 +438,11 @@ struct mb_plan {
   // host copies kept for the parity hooks (mb_plan_node_heights / mb_plan_gamma)
   std::vector<double> zslot, g2, s0;
   std::vector<double2> gd, gi;
+  // multi-device plan: one sub-plan per device that received pairs, the
+  // global pair index of each of its pairs, and its first structure
+  std::vector<mb_plan*> shards;
+  std::vector<std::vector<long>> shard_rows;
+  std::vector<int> shard_s0, shard_dev;
 };
 
 namespace {
@@ -923,20 +933,8 @@ void execute_plan(mb_plan* pl, cudaStream_t st) {
   pl->executed = true;
 }
 
-int collect_results(mb_plan* pl, double* eta, double* rho, mb_point_status* status) {
-  if (!pl->executed) fail(MB_ERR_ARG, "plan has not been executed");
-  cudaStream_t st = pl->ctx->stream;
-  const std::size_t ne = (std::size_t)pl->npairs * pl->n;
-  std::vector<mbx::PointStatus> stv((std::size_t)pl->npairs);
-  if (eta) cuda_check(cudaMemcpyAsync(eta, pl->prop.eta, ne * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H eta");
-  if (rho) cuda_check(cudaMemcpyAsync(rho, pl->prop.rho, ne * sizeof(double2), cudaMemcpyDeviceToHost, st), "D2H rho");
-  cuda_check(cudaMemcpyAsync(stv.data(), pl->prop.status, stv.size() * sizeof(mbx::PointStatus),
-                             cudaMemcpyDeviceToHost, st),
-             "D2H status");
-  cuda_check(cudaStreamSynchronize(st), "D2H");
-  if (status)
-    for (std::size_t i = 0; i < stv.size(); ++i)
-      status[i] = mb_point_status{stv[i].code, stv[i].step, stv[i].rhst, stv[i].reserved};
+// the first failing pair in row order decides (sweep.cpp:136-137)
+void raise_first_failure(const std::vector<mbx::PointStatus>& stv) {
   for (std::size_t i = 0; i < stv.size(); ++i) {
     if (stv[i].code == MB_POINT_OK) continue;
     const std::string where = " (pair " + std::to_string(i) + ", step " + std::to_string(stv[i].step) + ")";
@@ -950,7 +948,183 @@ int collect_results(mb_plan* pl, double* eta, double* rho, mb_point_status* stat
       fail(MB_ERR_CONVERGENCE, "bulk reflection did not settle within 10000 periods (pair " + std::to_string(i) + ")");
     fail(MB_ERR_BREAKDOWN, "reflection extraction: solve_right: singular or ill-conditioned system" + where);
   }
+}
+
+// D2H of one single-device plan's outputs (any pointer may be null)
+void fetch_results(mb_plan* pl, double* eta, double2* rho, std::vector<mbx::PointStatus>& stv) {
+  if (!pl->executed) fail(MB_ERR_ARG, "plan has not been executed");
+  cuda_check(cudaSetDevice(pl->ctx->device), "cudaSetDevice");
+  cudaStream_t st = pl->ctx->stream;
+  const std::size_t ne = (std::size_t)pl->npairs * pl->n;
+  stv.assign((std::size_t)pl->npairs, mbx::PointStatus{});
+  if (eta) cuda_check(cudaMemcpyAsync(eta, pl->prop.eta, ne * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H eta");
+  if (rho) cuda_check(cudaMemcpyAsync(rho, pl->prop.rho, ne * sizeof(double2), cudaMemcpyDeviceToHost, st), "D2H rho");
+  cuda_check(cudaMemcpyAsync(stv.data(), pl->prop.status, stv.size() * sizeof(mbx::PointStatus),
+                             cudaMemcpyDeviceToHost, st),
+             "D2H status");
+  cuda_check(cudaStreamSynchronize(st), "D2H");
+}
+
+int collect_results(mb_plan* pl, double* eta, double* rho, mb_point_status* status) {
+  std::vector<mbx::PointStatus> stv;
+  if (pl->shards.empty()) {
+    fetch_results(pl, eta, reinterpret_cast<double2*>(rho), stv);
+  } else {
+    // gather every shard's rows into the caller's preassigned rows (sweep.cpp:92-108)
+    stv.assign((std::size_t)pl->npairs, mbx::PointStatus{});
+    const int n = pl->n;
+    for (std::size_t s = 0; s < pl->shards.size(); ++s) {
+      mb_plan* sp = pl->shards[s];
+      const std::vector<long>& rows = pl->shard_rows[s];
+      std::vector<double> e(eta ? rows.size() * n : 0);
+      std::vector<double2> r(rho ? rows.size() * n : 0);
+      std::vector<mbx::PointStatus> ss;
+      fetch_results(sp, eta ? e.data() : nullptr, rho ? r.data() : nullptr, ss);
+      for (std::size_t i = 0; i < rows.size(); ++i) {
+        const long g = rows[i];
+        if (eta) std::memcpy(eta + (std::size_t)g * n, e.data() + i * n, n * sizeof(double));
+        if (rho) std::memcpy(rho + (std::size_t)g * n * 2, r.data() + i * n, n * sizeof(double2));
+        stv[(std::size_t)g] = ss[i];
+      }
+    }
+  }
+  if (status)
+    for (std::size_t i = 0; i < stv.size(); ++i)
+      status[i] = mb_point_status{stv[i].code, stv[i].step, stv[i].rhst, stv[i].reserved};
+  raise_first_failure(stv);
   return MB_OK;
+}
+
+// ------------------------------------------------------------ multi-device
+// pairs are independent and U depends only on the structure.
+// Several fields: contiguous structure blocks, balanced by pair count (a
+// structure's coefficient table is built on one device only). One field:
+// pairs round-robin. Fixed map, so the gathered rows do not depend on timing.
+mb_plan* create_multi_plan(mb_context* ctx, const mb_rods* rods, const mb_field* fields, int nfields, double gamma,
+                           const mb_pair* pairs, long npairs, const mb_stepper* stepper, const mb_options* opts) {
+  if (!pairs || !fields) fail(MB_ERR_ARG, "null argument");
+  if (nfields < 1 || npairs < 1) fail(MB_ERR_ARG, "need at least one field and one pair");
+  const int G = (int)ctx->subs.size();
+  std::vector<int> owner((std::size_t)npairs, 0);
+  std::vector<int> s_lo(G, 0), s_hi(G, 0);
+  if (nfields > 1) {
+    std::vector<long> cnt((std::size_t)nfields, 0);
+    for (long p = 0; p < npairs; ++p) {
+      const int s = pairs[p].structure;
+      if (s < 0 || s >= nfields) fail(MB_ERR_ARG, "pair: structure index out of range");
+      ++cnt[(std::size_t)s];
+    }
+    // device g takes structures whose cumulative pair count midpoint falls in [g, g+1) / G of the total
+    long acc = 0;
+    std::vector<int> dev_of((std::size_t)nfields, 0);
+    for (int s = 0; s < nfields; ++s) {
+      const double mid = (double)acc + 0.5 * (double)cnt[(std::size_t)s];
+      dev_of[(std::size_t)s] = std::min(G - 1, (int)(mid * G / (double)npairs));
+      acc += cnt[(std::size_t)s];
+    }
+    for (int g = 0; g < G; ++g) {
+      s_lo[g] = nfields;
+      s_hi[g] = 0;
+    }
+    for (int s = 0; s < nfields; ++s) {
+      const int g = dev_of[(std::size_t)s];
+      s_lo[g] = std::min(s_lo[g], s);
+      s_hi[g] = std::max(s_hi[g], s + 1);
+    }
+    for (long p = 0; p < npairs; ++p) owner[(std::size_t)p] = dev_of[(std::size_t)pairs[p].structure];
+  } else {
+    for (long p = 0; p < npairs; ++p) owner[(std::size_t)p] = (int)(p % G);
+    for (int g = 0; g < G; ++g) s_lo[g] = 0, s_hi[g] = 1;
+  }
+  auto* pl = new mb_plan();
+  pl->ctx = ctx;
+  pl->n = rods ? rods->n : 0;
+  pl->npairs = npairs;
+  pl->S = nfields;
+  try {
+    for (int g = 0; g < G; ++g) {
+      std::vector<mb_pair> mine;
+      std::vector<long> rows;
+      for (long p = 0; p < npairs; ++p)
+        if (owner[(std::size_t)p] == g) {
+          mb_pair q = pairs[p];
+          q.structure -= s_lo[g];
+          mine.push_back(q);
+          rows.push_back(p);
+        }
+      if (mine.empty()) continue;
+      mb_plan* sp = create_plan(ctx->subs[(std::size_t)g], rods, fields + s_lo[g], s_hi[g] - s_lo[g], gamma,
+                                mine.data(), (long)mine.size(), stepper, opts);
+      pl->shards.push_back(sp);
+      pl->shard_rows.push_back(std::move(rows));
+      pl->shard_s0.push_back(s_lo[g]);
+      pl->shard_dev.push_back(g);
+    }
+    for (mb_plan* sp : pl->shards) cuda_check(cudaStreamSynchronize(sp->ctx->stream), "plan upload");
+    const mb_plan* f = pl->shards.front();
+    pl->ndiff = f->ndiff;
+    pl->npad = f->npad;
+    pl->nslots = f->nslots;
+    for (mb_plan* sp : pl->shards) pl->h2d_bytes += sp->h2d_bytes;
+  } catch (...) {
+    for (mb_plan* sp : pl->shards) free_plan(sp);
+    delete pl;
+    throw;
+  }
+  return pl;
+}
+
+// one host thread per device; the first failure (shard order) is rethrown
+void execute_multi(mb_plan* pl) {
+  const std::size_t G = pl->shards.size();
+  std::vector<std::exception_ptr> err(G);
+  std::vector<std::thread> th;
+  for (std::size_t s = 0; s < G; ++s)
+    th.emplace_back([&, s] {
+      try {
+        execute_plan(pl->shards[s], nullptr);
+      } catch (...) {
+        err[s] = std::current_exception();
+      }
+    });
+  for (auto& t : th) t.join();
+  for (auto& e : err)
+    if (e) std::rethrow_exception(e);
+  pl->ms_total = pl->ms_pot = pl->ms_prop = 0.0f;
+  pl->launches = 0;
+  for (mb_plan* sp : pl->shards) {
+    pl->ms_total = std::max(pl->ms_total, sp->ms_total);
+    pl->ms_pot = std::max(pl->ms_pot, sp->ms_pot);
+    pl->ms_prop = std::max(pl->ms_prop, sp->ms_prop);
+    pl->launches += sp->launches;
+  }
+  pl->executed = true;
+}
+
+void destroy_any(mb_plan* pl) {
+  if (!pl) return;
+  if (!pl->shards.empty()) {
+    for (mb_plan* sp : pl->shards) free_plan(sp);
+    delete pl;
+    return;
+  }
+  free_plan(pl);
+}
+
+mb_plan* create_any(mb_context* ctx, const mb_rods* rods, const mb_field* fields, int nfields, double gamma,
+                    const mb_pair* pairs, long npairs, const mb_stepper* stepper, const mb_options* opts) {
+  if (!ctx) fail(MB_ERR_ARG, "null context");
+  if (!ctx->subs.empty()) return create_multi_plan(ctx, rods, fields, nfields, gamma, pairs, npairs, stepper, opts);
+  mb_plan* pl = create_plan(ctx, rods, fields, nfields, gamma, pairs, npairs, stepper, opts);
+  cuda_check(cudaStreamSynchronize(ctx->stream), "plan upload");
+  return pl;
+}
+
+void execute_any(mb_plan* pl, cudaStream_t st) {
+  if (!pl->shards.empty())
+    execute_multi(pl);
+  else
+    execute_plan(pl, st);
 }
 
 }  // namespace
@@ -1057,9 +1231,42 @@ int mb_context_create(int device, mb_context** out) {
   });
 }
 
+int mb_context_create_multi(const int* devices, int ndevices, mb_context** out) {
+  return guarded([&] {
+    if (!out || !devices || ndevices < 1) fail(MB_ERR_ARG, "mb_context_create_multi: need a device list");
+    *out = nullptr;
+    auto* ctx = new mb_context();
+    try {
+      for (int i = 0; i < ndevices; ++i) {
+        mb_context* sub = nullptr;
+        const int rc = mb_context_create(devices[i], &sub);
+        if (rc != MB_OK) fail(rc, g_last_error);
+        ctx->subs.push_back(sub);
+      }
+    } catch (...) {
+      for (mb_context* sub : ctx->subs) mb_context_destroy(sub);
+      delete ctx;
+      throw;
+    }
+    ctx->device = ctx->subs.front()->device;
+    ctx->stream = ctx->subs.front()->stream;
+    *out = ctx;
+  });
+}
+
+int mb_context_device_count(const mb_context* ctx) {
+  if (!ctx) return 0;
+  return ctx->subs.empty() ? 1 : (int)ctx->subs.size();
+}
+
 int mb_context_destroy(mb_context* ctx) {
   return guarded([&] {
     if (!ctx) return;
+    if (!ctx->subs.empty()) {
+      for (mb_context* sub : ctx->subs) mb_context_destroy(sub);
+      delete ctx;
+      return;
+    }
     cudaStreamSynchronize(ctx->stream);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
@@ -1073,8 +1280,7 @@ int mb_plan_create(mb_context* ctx, const mb_rods* rods, const mb_field* fields,
     if (!out || !ctx) fail(MB_ERR_ARG, "null argument");
     *out = nullptr;
     std::lock_guard<std::mutex> lk(ctx->mu);
-    *out = create_plan(ctx, rods, fields, nfields, gamma, pairs, npairs, stepper, opts);
-    cuda_check(cudaStreamSynchronize(ctx->stream), "plan upload");
+    *out = create_any(ctx, rods, fields, nfields, gamma, pairs, npairs, stepper, opts);
   });
 }
 
@@ -1082,7 +1288,7 @@ int mb_plan_execute(mb_plan* plan, void* stream) {
   return guarded([&] {
     if (!plan) fail(MB_ERR_ARG, "null plan");
     std::lock_guard<std::mutex> lk(plan->ctx->mu);
-    execute_plan(plan, static_cast<cudaStream_t>(stream));
+    execute_any(plan, static_cast<cudaStream_t>(stream));
   });
 }
 
@@ -1111,7 +1317,7 @@ int mb_plan_info(const mb_plan* plan, long* slots, int* ndiff, long* coef_bytes,
     if (!plan) fail(MB_ERR_ARG, "null plan");
     if (slots) *slots = plan->nslots;
     if (ndiff) *ndiff = plan->ndiff;
-    if (coef_bytes) *coef_bytes = (long)plan->S * plan->nslots * plan->ndiff * (long)sizeof(double2);
+    if (coef_bytes) *coef_bytes = (long)plan->S * plan->nslots * plan->ndiff * (long)sizeof(double2);  // all devices
     if (npad) *npad = plan->npad;
     if (h2d_bytes) *h2d_bytes = plan->h2d_bytes;
   });
@@ -1120,17 +1326,28 @@ int mb_plan_info(const mb_plan* plan, long* slots, int* ndiff, long* coef_bytes,
 int mb_plan_profile(const mb_plan* plan, double* cycles) {
   return guarded([&] {
     if (!plan || !cycles) fail(MB_ERR_ARG, "null argument");
-    unsigned long long v[12];
-    cuda_check(cudaMemcpy(v, plan->prop.prof, sizeof v, cudaMemcpyDeviceToHost), "D2H profile");
-    for (int q = 0; q < 12; ++q) cycles[q] = (double)v[q] / (double)plan->npairs;
+    double acc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    std::vector<const mb_plan*> parts;
+    if (plan->shards.empty())
+      parts.push_back(plan);
+    else
+      for (const mb_plan* sp : plan->shards) parts.push_back(sp);
+    for (const mb_plan* sp : parts) {
+      unsigned long long v[12];
+      cuda_check(cudaSetDevice(sp->ctx->device), "cudaSetDevice");
+      cuda_check(cudaMemcpy(v, sp->prop.prof, sizeof v, cudaMemcpyDeviceToHost), "D2H profile");
+      for (int q = 0; q < 12; ++q) acc[q] += (double)v[q];
+    }
+    for (int q = 0; q < 12; ++q) cycles[q] = acc[q] / (double)plan->npairs;
   });
 }
 
 int mb_plan_node_heights(const mb_plan* plan, double* z, long cap) {
   return guarded([&] {
     if (!plan || !z) fail(MB_ERR_ARG, "null argument");
-    if (cap < (long)plan->zslot.size()) fail(MB_ERR_ARG, "mb_plan_node_heights: capacity too small");
-    std::memcpy(z, plan->zslot.data(), plan->zslot.size() * sizeof(double));
+    const mb_plan* p0 = plan->shards.empty() ? plan : plan->shards.front();
+    if (cap < (long)p0->zslot.size()) fail(MB_ERR_ARG, "mb_plan_node_heights: capacity too small");
+    std::memcpy(z, p0->zslot.data(), p0->zslot.size() * sizeof(double));
   });
 }
 
@@ -1138,6 +1355,15 @@ int mb_plan_gamma(const mb_plan* plan, long pair, double* gdiag, double* ginv, d
   return guarded([&] {
     if (!plan) fail(MB_ERR_ARG, "null plan");
     if (pair < 0 || pair >= plan->npairs) fail(MB_ERR_ARG, "mb_plan_gamma: pair index out of range");
+    if (!plan->shards.empty()) {
+      for (std::size_t s = 0; s < plan->shards.size(); ++s) {
+        const auto& rows = plan->shard_rows[s];
+        auto it = std::lower_bound(rows.begin(), rows.end(), pair);
+        if (it != rows.end() && *it == pair)
+          return (void)mb_plan_gamma(plan->shards[s], (long)(it - rows.begin()), gdiag, ginv, gamma2, sin_theta0);
+      }
+      fail(MB_ERR_ARG, "mb_plan_gamma: pair not found");
+    }
     const std::size_t o = (std::size_t)pair * plan->n;
     for (int i = 0; i < plan->n; ++i) {
       if (gdiag) gdiag[2 * i] = plan->gd[o + i].x, gdiag[2 * i + 1] = plan->gd[o + i].y;
@@ -1153,6 +1379,17 @@ int mb_plan_coefficients(mb_plan* plan, int structure, double* coef, long cap) {
     if (!plan || !coef) fail(MB_ERR_ARG, "null argument");
     if (structure < 0 || structure >= plan->S) fail(MB_ERR_ARG, "mb_plan_coefficients: structure out of range");
     if (!plan->executed) fail(MB_ERR_ARG, "plan has not been executed");
+    if (!plan->shards.empty()) {
+      for (std::size_t s = 0; s < plan->shards.size(); ++s) {
+        const int lo = plan->shard_s0[s], hi = lo + plan->shards[s]->S;
+        if (structure >= lo && structure < hi) {
+          const int rc = mb_plan_coefficients(plan->shards[s], structure - lo, coef, cap);
+          if (rc != MB_OK) fail(rc, g_last_error);
+          return;
+        }
+      }
+      fail(MB_ERR_ARG, "mb_plan_coefficients: structure not on any device");
+    }
     const std::size_t cnt = (std::size_t)plan->nslots * plan->ndiff;
     if (cap < (long)(2 * cnt)) fail(MB_ERR_ARG, "mb_plan_coefficients: capacity too small");
     std::lock_guard<std::mutex> lk(plan->ctx->mu);
@@ -1167,7 +1404,7 @@ int mb_plan_destroy(mb_plan* plan) {
   return guarded([&] {
     if (!plan) return;
     std::lock_guard<std::mutex> lk(plan->ctx->mu);
-    free_plan(plan);
+    destroy_any(plan);
   });
 }
 
@@ -1192,8 +1429,8 @@ int mb_rocking_curve(mb_context* ctx, const mb_field* field, const mb_rods* rods
       for (int a = 0; a < n_theta0; ++a) pairs.push_back(mb_pair{0, theta0[a], theta1[b]});
     if (!ctx) fail(MB_ERR_ARG, "null context");
     std::lock_guard<std::mutex> lk(ctx->mu);
-    plan = create_plan(ctx, rods, field, 1, gamma, pairs.data(), (long)pairs.size(), stepper, opts);
-    execute_plan(plan, nullptr);
+    plan = create_any(ctx, rods, field, 1, gamma, pairs.data(), (long)pairs.size(), stepper, opts);
+    execute_any(plan, nullptr);
   });
   if (rc != MB_OK) {
     if (plan) mb_plan_destroy(plan);

@@ -108,3 +108,35 @@ def test_edge_cases():
     eta, _, st = mb.solve_batch(configs.product_fields(w), top, w.gamma, [(0, 1.0, 0.0)],
                                 mb.SweepOptions(method="sp6", slices=20))
     assert eta.shape == (1, 256) and (st["code"] == 0).all() and np.isfinite(eta).all()
+
+
+# ---------------------------------------------------------------- multi-device context
+@pytest.mark.parametrize("cfg", ["cfg0", "cfg2", "cfg4n127"])
+def test_multi_device_context_bitwise(cfg):
+    """One context over several device shards (here two or three shards on
+    the one GPU of the box, each with its own stream) gives bitwise the rows
+    of the single-device context, in pair order (test_sweep.cpp:55-68: any
+    thread count gives identical intensities)."""
+    if cfg == "cfg0":
+        w, path = configs.config0(), 0
+    elif cfg == "cfg2":
+        w, path = configs.config2(n_structures=24).subset(theta0=[0.5, 1.7, 3.9, 6.5], slices=200, z_bottom=-4.0), 0
+    else:
+        w, path = configs.config4(127, "sp6", n_structures=3).subset(theta0=[0.5, 2.5, 6.0], slices=60,
+                                                                    z_bottom=-0.96), 3
+    rods = mb.RodSet.build_first(mb.Lattice2D(w.a1, w.a2), w.n_rods)
+    opts = mb.SweepOptions(method=w.method, slices=w.slices, fsal=True, path=path)
+    pairs = [(s, t0, t1) for s in range(len(w.structures)) for t1 in w.theta1 for t0 in w.theta0]
+    fields = configs.product_fields(w)
+    one = mb.solve_batch(fields, rods, w.gamma, pairs, opts, mb.Context(0))
+    for devs in ([0, 0], [0, 0, 0]):
+        ctx = mb.Context(devices=devs)
+        many = mb.solve_batch(fields, rods, w.gamma, pairs, opts, ctx)
+        assert np.array_equal(one[0], many[0]) and np.array_equal(one[1], many[1])
+        assert np.array_equal(one[2]["rhst"], many[2]["rhst"])
+        ctx.close()
+    if len(w.structures) == 1:  # rocking_curve over a multi-device context: angles round-robin
+        grid = mb.AngleGrid.validated(w.theta0, w.theta1)
+        a = mb.rocking_curve(fields[0], rods, w.gamma, grid, opts, mb.Context(0))
+        b = mb.rocking_curve(fields[0], rods, w.gamma, grid, opts, mb.Context(devices=[0, 0]))
+        assert np.array_equal(a.eta, b.eta)
