@@ -88,7 +88,7 @@ __device__ __forceinline__ int ss(int r, int c) {
 }
 
 struct Layout {
-  size_t planes, boxes, fpub, tpub, tloc, wch, scr, g2s, rsum, dsum, pubv, occ, soff, sboxpos, total;
+  size_t planes, boxes, fpub, tpub, tloc, wch, scr, g2s, rsum, dsum, pubv, occ, soff, tbar, total;
 };
 
 __host__ __device__ inline size_t al16(size_t b) { return (b + 15) & ~(size_t)15; }
@@ -122,13 +122,14 @@ __host__ __device__ inline Layout cluster_layout(int np, int SW, int nq, int box
   o += al16((size_t)kMaxOcc * (4 * sizeof(double) + sizeof(int)));
   L.soff = o;
   o += al16((size_t)np * sizeof(int));
-  L.sboxpos = o;
-  o += al16((size_t)ndiff * sizeof(int));
+  L.tbar = o;  // TMA: box-full mbarriers [2], box-empty mbarriers [2] (cluster multicast)
+  o += al16(4 * sizeof(unsigned long long));
   L.total = o;
   return L;
 }
 
 // 3M box GEMM on the slab: acc = U[rows of the warp's blocks, :] * X[:, slab]
+// (MB_GEMM_4M builds: the 4-multiply form, for the 3M-vs-4M accuracy A/B)
 template <class C>
 __device__ __forceinline__ void slab_gemm(double (&acc)[C::MB][C::NB][4], const double2* __restrict__ box,
                                           const int* __restrict__ soff, const int (&raddr)[C::MB],
@@ -136,12 +137,20 @@ __device__ __forceinline__ void slab_gemm(double (&acc)[C::MB][C::NB][4], const 
                                           int lane, int kmax, int n) {
   const int kl = lane & 3, cl = lane >> 2;
   double t1[C::MB][C::NB][2], t2[C::MB][C::NB][2], t3[C::MB][C::NB][2];
+#ifdef MB_GEMM_4M
+  double t4[C::MB][C::NB][2];
+#endif
 #pragma unroll
   for (int m = 0; m < C::MB; ++m)
 #pragma unroll
     for (int nb = 0; nb < C::NB; ++nb)
 #pragma unroll
-      for (int e = 0; e < 2; ++e) t1[m][nb][e] = t2[m][nb][e] = t3[m][nb][e] = 0.0;
+      for (int e = 0; e < 2; ++e) {
+        t1[m][nb][e] = t2[m][nb][e] = t3[m][nb][e] = 0.0;
+#ifdef MB_GEMM_4M
+        t4[m][nb][e] = 0.0;
+#endif
+      }
 #pragma unroll 2
   for (int k0 = 0; k0 < kmax; k0 += 4) {
     const int k = k0 + kl;
@@ -159,6 +168,17 @@ __device__ __forceinline__ void slab_gemm(double (&acc)[C::MB][C::NB][4], const 
       if (8 * (warp + 8 * m) >= n) continue;  // warp-uniform: block of padding rows
       double2 a = make_double2(0.0, 0.0);
       if (raddr[m] >= 0) a = box[raddr[m] - offk];
+#ifdef MB_GEMM_4M
+#pragma unroll
+      for (int nb = 0; nb < C::NB; ++nb) dmma(t1[m][nb][0], t1[m][nb][1], a.x, br[nb]);
+#pragma unroll
+      for (int nb = 0; nb < C::NB; ++nb) dmma(t2[m][nb][0], t2[m][nb][1], a.y, bi[nb]);
+#pragma unroll
+      for (int nb = 0; nb < C::NB; ++nb) dmma(t3[m][nb][0], t3[m][nb][1], a.x, bi[nb]);
+#pragma unroll
+      for (int nb = 0; nb < C::NB; ++nb) dmma(t4[m][nb][0], t4[m][nb][1], a.y, br[nb]);
+      (void)bs;
+#else
       const double as = a.x + a.y;
 #pragma unroll
       for (int nb = 0; nb < C::NB; ++nb) dmma(t1[m][nb][0], t1[m][nb][1], a.x, br[nb]);
@@ -166,6 +186,7 @@ __device__ __forceinline__ void slab_gemm(double (&acc)[C::MB][C::NB][4], const 
       for (int nb = 0; nb < C::NB; ++nb) dmma(t2[m][nb][0], t2[m][nb][1], a.y, bi[nb]);
 #pragma unroll
       for (int nb = 0; nb < C::NB; ++nb) dmma(t3[m][nb][0], t3[m][nb][1], as, bs[nb]);
+#endif
     }
   }
 #pragma unroll
@@ -175,7 +196,11 @@ __device__ __forceinline__ void slab_gemm(double (&acc)[C::MB][C::NB][4], const 
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         acc[m][nb][e] = t1[m][nb][e] - t2[m][nb][e];
+#ifdef MB_GEMM_4M
+        acc[m][nb][2 + e] = t3[m][nb][e] + t4[m][nb][e];
+#else
         acc[m][nb][2 + e] = (t3[m][nb][e] - t1[m][nb][e]) - t2[m][nb][e];
+#endif
       }
 }
 
@@ -257,7 +282,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
   double* const bdrift = bkick + kMaxOcc;                            // (bulk window: h_bulk)
   int* const onode = reinterpret_cast<int*>(bdrift + kMaxOcc);
   int* const soff = reinterpret_cast<int*>(smem + LY.soff);
-  int* const sboxpos = reinterpret_cast<int*>(smem + LY.sboxpos);
+  unsigned long long* const tfull = reinterpret_cast<unsigned long long*>(smem + LY.tbar);  // [2]
   // slab planes: X0, X1 (, X2) re/im
   double* const X0r = planes;
   double* const X0i = planes + PL;
@@ -313,7 +338,11 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
   // per-pair L2 scratch: M0 (A), M1 (B), row-major NP x NP planes
   const long NN = (long)NP * NP;
   const int kmax = (n + 3) & ~3;
-  for (int i = tid; i < p.ndiff; i += CNT) sboxpos[i] = p.boxpos[i];
+  if (tid == 0) {
+    mbar_init(tfull + 0, 1);
+    mbar_init(tfull + 1, 1);
+    mbar_fence_init();
+  }
   if (tid == 0) *reinterpret_cast<volatile int*>(tpub + 3 * SW) = 0;  // panel flag
   for (int i = tid; i < kMaxOcc; i += CNT) {
     okick[i] = p.occ_kick[i];
@@ -323,8 +352,11 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
     onode[i] = p.occ_node[i];
   }
   // box holes are read for the padded k in [n, kmax) (times zero rows of X):
-  // keep them zero, never stale shared memory
-  for (int i = tid; i < 2 * p.box_size; i += CNT) boxes[i] = make_double2(0.0, 0.0);
+  // the boxed table carries them as zeros, every staged box is complete.
+  // TMA state per box buffer (CTA-uniform, monotone over the pairs): a copy
+  // in flight, and the mbarrier parity to wait for
+  unsigned tpend = 0u, tph = 0u;
+  const unsigned box_bytes = (unsigned)p.box_size * (unsigned)sizeof(double2);
   for (int i = tid; i < NP; i += CNT) soff[i] = i < n ? p.rowoff[i] : 0;
   int solve_id = 0;  // monotone over the pairs: panel flags are never reset
 
@@ -345,7 +377,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
   // M3: the own Q slab saved across a bulk period's reflection read
   double* const M3r = M0r + 6 * NN;
   double* const M3i = M0r + 7 * NN;
-  const double2* coef = p.coef + (long)p.pair_struct[pair] * p.nslots * p.ndiff;
+  const double2* coef = p.coef + (long)p.pair_struct[pair] * p.nslots * p.box_size;
   for (int i = tid; i < NP; i += CNT) g2s[i] = i < n ? p.gamma2[pair * n + i] : 0.0;
 
   // own elements: block m -> rows 8 (warp + 8 m) + lane/4, block nb -> slab
@@ -415,10 +447,23 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
   auto wkick = [&](int r) -> double { return (BULK && bulk_phase) ? bkick[r] : okick[r]; };
   auto wdrift = [&](int r) -> double { return (BULK && bulk_phase) ? bdrift[r] : odrift[r]; };
   auto slot_of = [&](int step, int r) -> long { return wbase() + (long)step * p.slot_stride + onode[r]; };
+  // TMA staging of one node's box: thread 0 arms the buffer's mbarrier and
+  // issues a single cp.async.bulk; every thread waits on the phase
   auto issue = [&](double2* dst, long slot) {
-    const double2* src = coef + slot * p.ndiff;
-    for (int d = tid; d < p.ndiff; d += CNT) cp_async16(dst + sboxpos[d], src + d);
-    cp_async_commit();
+    const int b = dst == boxes ? 0 : 1;
+    if (tid == 0) {
+      mbar_expect_tx(tfull + b, box_bytes);
+      bulk_g2s(dst, coef + slot * p.box_size, box_bytes, tfull + b);
+    }
+    tpend |= 1u << b;
+  };
+  auto wait_box = [&](double2* buf) {
+    const int b = buf == boxes ? 0 : 1;
+    if ((tpend >> b) & 1u) {
+      mbar_wait(tfull + b, (tph >> b) & 1u);
+      tph ^= 1u << b;
+      tpend &= ~(1u << b);
+    }
   };
   double2* cur = boxes;
   double2* nxt = boxes + p.box_size;
@@ -433,8 +478,8 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
 
   auto begin_occ = [&](int nstep, int nr) -> double2* {
     CPROF(2);
-    cp_async_wait_all();
-    __syncthreads();
+    wait_box(cur);
+    __syncthreads();  // every warp is done with nxt (its previous box)
     CPROF(0);
     if (nstep < L) {
       const long ns = slot_of(nstep, nr);
@@ -1184,7 +1229,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
       const double xi = n == 0 ? 1.0 : (ND > 0.0 ? inf_d() : H / Lo);
       if (xi > p.threshold) {
         // P <- P Q^-1, Q <- I (proposed.cpp:196-202)
-        cp_async_wait_all();  // the prefetched box of the next occurrence stays in its buffer
+        // the prefetched box of the next occurrence stays in flight into its buffer
         const bool main = !(BULK && bulk_phase);  // SolveStats counts the slab solve only (proposed.cpp:328)
         if (main && !isfinite(xi)) ++npiv;
         CPROF(4);
@@ -1238,7 +1283,8 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
       CPROF(4);
     }
   }
-  cp_async_wait_all();
+  wait_box(boxes);  // no copy may stay in flight past the window
+  wait_box(boxes + p.box_size);
   __syncthreads();
   if (code) break;
 

@@ -438,6 +438,8 @@ struct mb_plan {
   // host copies kept for the parity hooks (mb_plan_node_heights / mb_plan_gamma)
   std::vector<double> zslot, g2, s0;
   std::vector<double2> gd, gi;
+  std::vector<int> boxpos;
+  int box_size = 0;
   // multi-device plan: one sub-plan per device that received pairs, the
   // global pair index of each of its pairs, and its first structure
   std::vector<mb_plan*> shards;
@@ -646,10 +648,17 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
     pl->s0 = s0;
     pl->gd = gd;
     pl->gi = gi;
+    pl->boxpos = boxpos;
+    pl->box_size = box_size;
     cudaStream_t st = ctx->stream;
 
-    // ---- coefficient table: K1 terms (atoms / gaussian layers) or host table
-    double2* coef = dev_alloc<double2>(pl, (std::size_t)nfields * nslots * ndiff);
+    // ---- coefficient table, boxed: slot = box_size double2 with difference d
+    // at boxpos[d] and zero holes (zeroed once here; K1 only writes the
+    // difference positions), so a node is one contiguous TMA bulk copy
+    const int* boxpos_dev = dev_upload(pl, boxpos.data(), boxpos.size());
+    const std::size_t coef_count = (std::size_t)nfields * nslots * box_size;
+    double2* coef = dev_alloc<double2>(pl, coef_count);
+    cuda_check(cudaMemsetAsync(coef, 0, coef_count * sizeof(double2), st), "zero the coefficient table");
     const int kind = fields[0].kind;
     if (kind == MB_FIELD_ATOMS || kind == MB_FIELD_GAUSSIAN_LAYERS) {
       int T = 0;
@@ -709,9 +718,11 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
       pp.term_xy = dev_upload(pl, xy.data(), xy.size());
       pp.amp = dev_alloc<double2>(pl, (std::size_t)nfields * T * ndiff);
       pp.coef = coef;
+      pp.boxpos = boxpos_dev;
+      pp.box_size = box_size;
     } else {
       // zero or tabulated: node-slot table evaluated on the host once
-      pl->host_coef.assign((std::size_t)nfields * nslots * ndiff, make_double2(0.0, 0.0));
+      pl->host_coef.assign(coef_count, make_double2(0.0, 0.0));
       if (kind == MB_FIELD_TABULATED) {
         RodTables rt;
         for (int d = 0; d < ndiff; ++d) rt.diff_m.push_back({rods->diff_m[2 * d], rods->diff_m[2 * d + 1]});
@@ -722,7 +733,8 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
           for (long sl = 0; sl < nslots; ++sl) {
             eval_tabulated(tb, zb, zslot[(std::size_t)sl], row.data());
             for (int d = 0; d < ndiff; ++d)
-              pl->host_coef[((std::size_t)f * nslots + sl) * ndiff + d] = make_double2(row[d].real(), row[d].imag());
+              pl->host_coef[((std::size_t)f * nslots + sl) * box_size + boxpos[(std::size_t)d]] =
+                  make_double2(row[d].real(), row[d].imag());
           }
         }
       }
@@ -1317,7 +1329,9 @@ int mb_plan_info(const mb_plan* plan, long* slots, int* ndiff, long* coef_bytes,
     if (!plan) fail(MB_ERR_ARG, "null plan");
     if (slots) *slots = plan->nslots;
     if (ndiff) *ndiff = plan->ndiff;
-    if (coef_bytes) *coef_bytes = (long)plan->S * plan->nslots * plan->ndiff * (long)sizeof(double2);  // all devices
+    // the boxed table's bytes over all devices
+    const int bs = plan->shards.empty() ? plan->box_size : plan->shards.front()->box_size;
+    if (coef_bytes) *coef_bytes = (long)plan->S * plan->nslots * bs * (long)sizeof(double2);
     if (npad) *npad = plan->npad;
     if (h2d_bytes) *h2d_bytes = plan->h2d_bytes;
   });
@@ -1393,10 +1407,20 @@ int mb_plan_coefficients(mb_plan* plan, int structure, double* coef, long cap) {
     const std::size_t cnt = (std::size_t)plan->nslots * plan->ndiff;
     if (cap < (long)(2 * cnt)) fail(MB_ERR_ARG, "mb_plan_coefficients: capacity too small");
     std::lock_guard<std::mutex> lk(plan->ctx->mu);
-    cuda_check(cudaMemcpyAsync(coef, plan->prop.coef + (std::size_t)structure * cnt, cnt * sizeof(double2),
+    const std::size_t bcnt = (std::size_t)plan->nslots * plan->box_size;
+    std::vector<double2> boxed(bcnt);
+    cuda_check(cudaSetDevice(plan->ctx->device), "cudaSetDevice");
+    cuda_check(cudaMemcpyAsync(boxed.data(), plan->prop.coef + (std::size_t)structure * bcnt, bcnt * sizeof(double2),
                                cudaMemcpyDeviceToHost, plan->ctx->stream),
                "D2H coefficient table");
     cuda_check(cudaStreamSynchronize(plan->ctx->stream), "D2H coefficient table");
+    // the boxed table back in difference order [slot][ndiff]
+    for (long sl = 0; sl < plan->nslots; ++sl)
+      for (int d = 0; d < plan->ndiff; ++d) {
+        const double2 v = boxed[(std::size_t)sl * plan->box_size + plan->boxpos[(std::size_t)d]];
+        coef[2 * ((std::size_t)sl * plan->ndiff + d)] = v.x;
+        coef[2 * ((std::size_t)sl * plan->ndiff + d) + 1] = v.y;
+      }
   });
 }
 

@@ -31,7 +31,12 @@ struct PotentialParams {
   const double2* term_cpre;  // complex prefactor
   const double2* term_xy;    // in-plane position (atoms) or (0,0)
   double2* amp;              // [S][T][ndiff] scratch
-  double2* coef;             // [S][nslots][ndiff]
+  // boxed table: coef[s][slot][box_size], difference d at position boxpos[d],
+  // holes zero (set once at plan creation): one node = one contiguous block
+  // that the propagation kernels stage with a single TMA bulk copy
+  double2* coef;             // [S][nslots][box_size]
+  const int* boxpos;         // [ndiff]
+  int box_size;
 };
 
 // ---- K2: propagation + RHST + extraction + intensity -----------------------
@@ -40,9 +45,9 @@ struct PropagateParams {
   int nsteps;
   long nslots;
   long npairs;
-  // coefficient table and its box scatter
-  const double2* coef;     // [S][nslots][ndiff]
-  const int* boxpos;       // [ndiff] -> position inside the smem box table
+  // coefficient table, boxed: node slot = box_size double2 (holes zero)
+  const double2* coef;     // [S][nslots][box_size]
+  const int* boxpos;       // [ndiff] -> position inside the box
   const int* rowoff;       // [n] -> m1*W2 + m2 (box row offset of rod j)
   int box_size, box_center;
   // pairs

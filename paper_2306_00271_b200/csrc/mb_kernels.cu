@@ -62,7 +62,7 @@ __global__ void potential_amp_kernel(const __grid_constant__ PotentialParams p) 
   }
 }
 
-// coef[s][slot][d] = sum_t amp[s][t][d] * exp(-alpha_t (z_slot - zc_t)^2)
+// coef[s][slot][boxpos[d]] = sum_t amp[s][t][d] * exp(-alpha_t (z_slot - zc_t)^2)
 // grid: (slot blocks of kSlotTile, S); threads over d. The z-Gaussians of the
 // slot tile are staged in shared memory; every amp element is read once per
 // tile and reused kSlotTile times from registers.
@@ -96,10 +96,10 @@ __global__ void __launch_bounds__(128) potential_coef_kernel(const __grid_consta
         im[q] = fma(a.y, g, im[q]);
       }
     }
-    double2* out = p.coef + ((long)s * p.nslots + slot0) * p.ndiff + d;
+    double2* out = p.coef + ((long)s * p.nslots + slot0) * p.box_size + p.boxpos[d];
 #pragma unroll
     for (int q = 0; q < kSlotTile; ++q)
-      if (q < nsl) out[(long)q * p.ndiff] = make_double2(re[q], im[q]);
+      if (q < nsl) out[(long)q * p.box_size] = make_double2(re[q], im[q]);
   }
 }
 
@@ -498,14 +498,15 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
   double* bkick = odrift + kMaxOcc;                   // [kMaxOcc] bulk window (h_bulk)
   double* bdrift = bkick + kMaxOcc;                   // [kMaxOcc]
   int* onode = reinterpret_cast<int*>(bdrift + kMaxOcc);
-  int* sboxpos = onode + kMaxOcc;  // [ndiff]
+  // TMA: one box-full mbarrier per box buffer (2 per column group)
+  unsigned long long* const tbar = reinterpret_cast<unsigned long long*>(onode + kMaxOcc);  // [2 WN]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = p.n;
   const long pair = blockIdx.x;
   const int wm = warp / C::WN, wn = warp % C::WN;
   Own<C> own{wm * C::TM, wn * C::TN, lane};
-  const double2* coef = p.coef + (long)p.pair_struct[pair] * p.nslots * p.ndiff;
+  const double2* coef = p.coef + (long)p.pair_struct[pair] * p.nslots * p.box_size;
   const int gtid = wm * 32 + lane;  // thread index inside the column group
   constexpr int GNT = C::NT / C::WN;
   auto group_sync = [&]() {
@@ -529,7 +530,6 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
   double* As = Xr[2];
   double* Ns = Xi[2];
   constexpr bool XS = !RK4 && NP >= 64;  // measured: a small gain at NP = 64 only
-  for (int i = tid; i < p.ndiff; i += C::NT) sboxpos[i] = p.boxpos[i];
   for (int i = tid; i < kMaxOcc; i += C::NT) {
     okick[i] = p.occ_kick[i];
     odrift[i] = p.occ_drift[i];
@@ -538,8 +538,12 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
     onode[i] = p.occ_node[i];
   }
   // box holes (positions no rod difference maps to) are read for the padded
-  // k in [n, kmax) and multiplied by zero rows of X: keep them zero, not stale
-  for (int i = tid; i < 2 * C::WN * p.box_size; i += C::NT) boxes[i] = make_double2(0.0, 0.0);
+  // k in [n, kmax) and multiplied by zero rows of X: the boxed table carries
+  // them as zeros, so every staged box is complete
+  if (tid == 0) {
+    for (int i = 0; i < 2 * C::WN; ++i) mbar_init(tbar + i, 1);
+    mbar_fence_init();
+  }
   for (int i = tid; i < NP; i += C::NT) {
     soff[i] = i < n ? p.rowoff[i] : 0;
     g2s[i] = i < n ? p.gamma2[pair * n + i] : 0.0;
@@ -594,14 +598,33 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
   auto wdrift = [&](int r) -> double { return (BULK && bulk_phase) ? bdrift[r] : odrift[r]; };
   // table pipeline: slot of occurrence (step, r) = base + step*stride + node
   auto slot_of = [&](int step, int r) -> long { return wbase() + (long)step * p.slot_stride + onode[r]; };
+  // TMA staging: the group's first thread arms the buffer's mbarrier with the
+  // byte count and issues one cp.async.bulk of the node's box; every thread
+  // of the group waits on the phase before reading. pend / ph: per buffer,
+  // a copy in flight / the parity to wait for (group-uniform).
+  double2* const bufA = boxes + (2 * wn) * p.box_size;
+  unsigned long long* const barA = tbar + 2 * wn;
+  const unsigned box_bytes = (unsigned)p.box_size * (unsigned)sizeof(double2);
+  unsigned pend = 0u, ph = 0u;
   auto issue = [&](double2* dst, long slot) {
-    const double2* src = coef + slot * p.ndiff;
-    for (int d = gtid; d < p.ndiff; d += GNT) cp_async16(dst + sboxpos[d], src + d);
-    cp_async_commit();
+    const int b = dst == bufA ? 0 : 1;
+    if (gtid == 0) {
+      mbar_expect_tx(barA + b, box_bytes);
+      bulk_g2s(dst, coef + slot * p.box_size, box_bytes, barA + b);
+    }
+    pend |= 1u << b;
   };
-  double2* cur = boxes + (2 * wn) * p.box_size;
-  double2* nxt = cur + p.box_size;
-  __syncthreads();  // sboxpos ready
+  auto wait_box = [&](double2* buf) {
+    const int b = buf == bufA ? 0 : 1;
+    if ((pend >> b) & 1u) {
+      mbar_wait(barA + b, (ph >> b) & 1u);
+      ph ^= 1u << b;
+      pend &= ~(1u << b);
+    }
+  };
+  double2* cur = bufA;
+  double2* nxt = bufA + p.box_size;
+  __syncthreads();  // barriers initialised
   long cur_slot = -1;
 
   int rhst = 0, npiv = 0;
@@ -613,8 +636,8 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
   // table of occurrence (step, r); prefetches the next occurrence's table.
   auto begin_occ = [&](int nstep, int nr) -> double2* {
     PROF_MARK(2);
-    cp_async_wait_all();
-    group_sync();
+    wait_box(cur);
+    group_sync();  // every warp of the group is done with nxt (its previous box)
     PROF_MARK(0);
     if (nstep < WL()) {
       const long ns = slot_of(nstep, nr);
@@ -930,7 +953,8 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
     }
     PROF_MARK(5);
   }
-  cp_async_wait_all();
+  wait_box(bufA);  // no copy may stay in flight past the window
+  wait_box(bufA + p.box_size);
   __syncthreads();
   if (code) break;
 
@@ -1111,7 +1135,7 @@ static size_t smem_bytes(const PropagateParams& p) {
   b += (size_t)np * sizeof(int);                      // soff
   b += sizeof(Scratch) + sizeof(PanelScratch) + 16;
   b += (size_t)kMaxOcc * (4 * sizeof(double) + sizeof(int));  // stepper tables (main, bulk)
-  b += (size_t)p.ndiff * sizeof(int);
+  b += 2 * (size_t)C::WN * sizeof(unsigned long long);         // TMA box barriers
   return b;
 }
 

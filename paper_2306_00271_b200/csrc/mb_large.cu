@@ -38,7 +38,8 @@ __device__ __forceinline__ int epi_sw(int r, int c) { return r * BN + (c ^ ((r &
 
 // byte offset of the epilogue tiles in the stage kernel's dynamic smem
 __host__ __device__ inline size_t epi_offset(const BigParams& p) {
-  const size_t b = 4 * KC * BN * sizeof(double) + (size_t)p.box_size * sizeof(double2) + (size_t)p.np * sizeof(int);
+  const size_t b = 4 * KC * BN * sizeof(double) + (size_t)p.box_size * sizeof(double2) + (size_t)p.np * sizeof(int) +
+                   16;  // + the box's TMA mbarrier
   return (b + 15) & ~(size_t)15;
 }
 
@@ -53,6 +54,7 @@ __global__ void __launch_bounds__(NTH, 2) big_stage_kernel(const __grid_constant
   double* xp = reinterpret_cast<double*>(smem);                 // [2 buf][2 plane][KC*BN]
   double2* box = reinterpret_cast<double2*>(xp + 4 * KC * BN);  // [box_size]
   int* soff = reinterpret_cast<int*>(box + p.box_size);         // [np]
+  unsigned long long* tbar = reinterpret_cast<unsigned long long*>(soff + p.np);  // np % 8 == 0: aligned
   // epilogue operand tiles (X = op, P) prefetched during the last K chunk:
   // [2 operand][2 plane][BM][BN], rows swizzled by epi_sw
   double* epi = reinterpret_cast<double*>(smem + epi_offset(p));
@@ -66,8 +68,15 @@ __global__ void __launch_bounds__(NTH, 2) big_stage_kernel(const __grid_constant
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp >> 1, wn = warp & 1;
 
-  const double2* coef = p.coef + ((long)p.pair_struct[pair] * p.nslots + s.slot) * p.ndiff;
-  for (int d = tid; d < p.ndiff; d += NTH) cp_async16(box + p.boxpos[d], coef + d);
+  // the node's box (holes zero in the boxed table): one TMA bulk copy
+  const double2* coef = p.coef + ((long)p.pair_struct[pair] * p.nslots + s.slot) * p.box_size;
+  const unsigned box_bytes = (unsigned)p.box_size * (unsigned)sizeof(double2);
+  if (tid == 0) {
+    mbar_init(tbar, 1);
+    mbar_fence_init();
+    mbar_expect_tx(tbar, box_bytes);
+    bulk_g2s(box, coef, box_bytes, tbar);
+  }
   for (int i = tid; i < np; i += NTH) soff[i] = i < n ? p.rowoff[i] : 0;
   const double* X = mat(p, pair, s.op);
   const int nck = (np + KC - 1) / KC;
@@ -118,6 +127,7 @@ __global__ void __launch_bounds__(NTH, 2) big_stage_kernel(const __grid_constant
   for (int kc = 0; kc < nck; ++kc) {
     cp_async_wait_all();
     __syncthreads();
+    if (kc == 0) mbar_wait(tbar, 0);  // the box has landed (barrier initialised before the sync)
     if (kc + 1 < nck)
       stage(kc + 1, (kc + 1) & 1);
     else

@@ -1,0 +1,72 @@
+"""cfg3 (N=199, 10 A, 1000 slices, 61 angles) accuracy study: how far apart
+two correct implementations of the reference algorithm land at full depth,
+and where the device sits among them (the noise floor at
+the SAME RHST schedule, and a 3M-vs-4M A/B of the complex GEMM).
+
+  python tools/cfg3_accuracy.py run --role dev3m    --out gpurun_out/a_dev3m.npz
+  MB_LIB=.../libmanybeam_b200_4m.so python tools/cfg3_accuracy.py run --role dev4m --out ...
+  python tools/cfg3_accuracy.py run --role ref      --out ...   (oracle/_ref, threshold 1000)
+  python tools/cfg3_accuracy.py run --role ref1500  --out ...   (oracle/_ref, threshold 1500)
+  python tools/cfg3_accuracy.py run --role port     --out ...   (restatement, oracle/_build)
+  python tools/cfg3_accuracy.py report a_*.npz  > profiles/cfg3_accuracy_r02.json
+"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path[:0] = [ROOT, os.path.join(ROOT, "tests"), os.path.join(ROOT, "oracle", "_ref"),
+                os.path.join(ROOT, "oracle", "_build")]
+
+
+def run(role, out, slices=None):
+    import harness as H
+    from paper_2306_00271_b200 import configs
+    w = configs.config3()
+    t0 = time.time()
+    if role.startswith("dev"):
+        eta, rho, st = H.run_device(w, fsal=True)
+        rh = st["rhst"]
+    elif role.startswith("ref"):
+        import mb_ref
+        thr = 1500.0 if role == "ref1500" else 1000.0
+        eta, rho, rh = H.run_oracle(mb_ref, w, threads=0, threshold=thr)
+    else:
+        import mb_oracle
+        eta, rho, rh = H.run_oracle(mb_oracle, w, threads=0)
+    np.savez_compressed(out, eta=eta, rho=rho, rhst=np.asarray(rh), role=role, seconds=time.time() - t0)
+    print(role, "done", time.time() - t0, flush=True)
+
+
+def report(paths):
+    import harness as H
+    d = {str(np.load(p)["role"]): np.load(p) for p in paths}
+    want = d["ref"]["eta"]
+    out = {"workload": "cfg3-manybeam-N199-sp6 (full: 61 angles, 1000 slices)", "against": "ref (oracle/_ref, threshold 1000)",
+           "rows": {}}
+    for k, v in d.items():
+        if k == "ref":
+            continue
+        e = v["eta"]
+        rows = np.linalg.norm(e - want, axis=1) / np.linalg.norm(want, axis=1).max()
+        out["rows"][k] = {"curve_error": H.curve_err(e, want),
+                          "entry_rel_err_floor_1e-12": H.entry_rel_err(e, want, 1e-12),
+                          "entry_rel_err_floor_1e-10": H.entry_rel_err(e, want, 1e-10),
+                          "entry_rel_err_floor_1e-6": H.entry_rel_err(e, want, 1e-6),
+                          "rhst_differs_at_angles": np.nonzero(v["rhst"] != d["ref"]["rhst"])[0].tolist(),
+                          "worst_angles": np.argsort(rows)[::-1][:5].tolist(),
+                          "worst_angle_errors": np.sort(rows)[::-1][:5].tolist()}
+    if "dev3m" in d and "dev4m" in d:
+        out["dev3m_vs_dev4m_curve_error"] = H.curve_err(d["dev3m"]["eta"], d["dev4m"]["eta"])
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "run":
+        args = dict(zip(sys.argv[2::2], sys.argv[3::2]))
+        run(args["--role"], args["--out"])
+    else:
+        report(sys.argv[2:])
