@@ -44,6 +44,7 @@ extern "C" {
 #define MB_POINT_EXTRACTION 3  /* "reflection extraction: ..." (zero pivot) */
 #define MB_POINT_BULK_READ 4   /* "bulk reflection read: ..." (BreakdownError, step = period) */
 #define MB_POINT_BULK_CONVERGENCE 5 /* ConvergenceError: bulk R did not settle (proposed.cpp:338-341) */
+#define MB_POINT_RECURSION 6   /* conventional method: "conventional recursion: ..." (conventional.cpp:67-74) */
 
 typedef struct mb_context mb_context;
 typedef struct mb_plan mb_plan;
@@ -127,6 +128,9 @@ int mb_beam_from_energy(double energy_ev, double* gamma, double* gamma_L);
 /* ---- stepper (proposed.hpp:23-43, splitting_coefficients.cpp) -------- */
 #define MB_STEP_RK4 0
 #define MB_STEP_SPLITTING 1
+#define MB_STEP_CONVENTIONAL 2 /* the multi-slice method (conventional.cpp:50-78): Pade-13
+                                  slice exponentials + reflection recursion; N <= 32,
+                                  no bulk seed; the other mb_stepper fields are unused */
 #define MB_SPLIT_ABA 0
 #define MB_SPLIT_BAB 1
 typedef struct {
@@ -138,8 +142,9 @@ typedef struct {
   const double* kick;
 } mb_stepper;
 
-/* StepperSpec::by_name (proposed.cpp:24-29): "rk4", "sp4", "sp6". The
- * coefficient arrays point to library-owned static storage. */
+/* StepperSpec::by_name (proposed.cpp:24-29): "rk4", "sp4", "sp6"; and the
+ * sweep's method name "conventional" (sweep.cpp:41-50) as MB_STEP_CONVENTIONAL.
+ * The coefficient arrays point to library-owned static storage. */
 int mb_stepper_by_name(const char* name, mb_stepper* out);
 
 /* ---- solve options (sweep.hpp:26-32, proposed.hpp:90-92) --------------- */

@@ -257,6 +257,7 @@ struct SweepOptions {
   bool residual_check = true;
   bool fsal = false;
   int device = 0;
+  std::vector<int> devices;  // EXTENSION: several GPUs behind one context (mb_context_create_multi)
 };
 
 // curve.hpp:19-31
@@ -291,6 +292,27 @@ inline mb_context* context(int device) {
   return ctx[(std::size_t)device]->c;
 }
 
+// a multi-device context per process and device list, created on first use
+inline mb_context* context(const std::vector<int>& devices) {
+  if (devices.empty()) return context(0);
+  if (devices.size() == 1) return context(devices.front());
+  struct Holder {
+    std::vector<int> devs;
+    mb_context* c = nullptr;
+    ~Holder() {
+      if (c) mb_context_destroy(c);
+    }
+  };
+  static thread_local std::vector<std::unique_ptr<Holder>> ctx;
+  for (auto& h : ctx)
+    if (h->devs == devices) return h->c;
+  auto h = std::make_unique<Holder>();
+  h->devs = devices;
+  check(mb_context_create_multi(devices.data(), (int)devices.size(), &h->c));
+  ctx.push_back(std::move(h));
+  return ctx.back()->c;
+}
+
 // sweep.hpp:37-38
 inline RockingCurve rocking_curve(const PotentialField& field, const RodSet& rods, double gamma,
                                   const AngleGrid& grid, const SweepOptions& opts) {
@@ -315,7 +337,8 @@ inline RockingCurve rocking_curve(const PotentialField& field, const RodSet& rod
     c.rod_labels.push_back("(" + std::to_string(rods.m(i)[0]) + ";" + std::to_string(rods.m(i)[1]) + ")");
   const mb_field f = field.view();
   const mb_rods r = rods.view();
-  const int rc = mb_rocking_curve(context(opts.device), &f, &r, gamma, grid.theta0.data(), (int)grid.theta0.size(),
+  mb_context* ctx = opts.devices.empty() ? context(opts.device) : context(opts.devices);
+  const int rc = mb_rocking_curve(ctx, &f, &r, gamma, grid.theta0.data(), (int)grid.theta0.size(),
                                   grid.theta1.data(), (int)grid.theta1.size(), &st, &o, c.eta.data(),
                                   reinterpret_cast<double*>(c.rho.data()), c.status.data());
   std::size_t step = 0;

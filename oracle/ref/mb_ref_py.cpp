@@ -155,9 +155,10 @@ void collect_nodes(const mb::StepWindow& w, const mb::NodeSchedule& s, std::vect
 
 // Materialise the reference field for one solve configuration.
 mb::PotentialField realise(const RefField& f, const mb::RodSet& rods, const mb::SlicingPlan& plan,
-                           const mb::StepperSpec& spec, double dz, int threads) {
+                           const mb::StepperSpec* spec, double dz, int threads) {
   if (f.direct) return *f.direct;
-  const mb::NodeSchedule sched = mb::schedule_for(spec);
+  // the conventional method evaluates at slice midpoints (conventional.cpp:56)
+  const mb::NodeSchedule sched = spec ? mb::schedule_for(*spec) : mb::midpoint_schedule();
   std::vector<double> zs;
   collect_nodes(mb::StepWindow::of_plan(plan), sched, zs);
   if (f.bulk_period) {
@@ -215,7 +216,12 @@ struct Opts {
   std::optional<mb::StepperSpec> stepper;
 };
 
-const mb::StepperSpec& spec_of(const Opts& o) { return o.stepper ? *o.stepper : mb::StepperSpec::by_name(o.method); }
+bool conventional(const Opts& o) { return !o.stepper && o.method == "conventional"; }
+// nullptr for the conventional method (sweep.cpp:41-50)
+const mb::StepperSpec* spec_of(const Opts& o) {
+  if (conventional(o)) return nullptr;
+  return o.stepper ? &*o.stepper : &mb::StepperSpec::by_name(o.method);
+}
 
 mb::SlicingPlan plan_of(const RefField& f, const Opts& o) {
   const mb::SlicingPlan plan = mb::SlicingPlan::with_target_dz(f.z_bottom, o.dz);
@@ -240,7 +246,7 @@ struct Rows {
 // sweep.cpp:54-143 with the per-row body of :89-109, keeping rho and SolveStats.
 Rows solve_rows(const RefField& field, const mb::RodSet& rods, double gamma, const mb::AngleGrid& grid,
                 const Opts& o) {
-  const mb::StepperSpec& spec = spec_of(o);
+  const mb::StepperSpec* spec = spec_of(o);
   const mb::SlicingPlan plan = plan_of(field, o);
   const mb::PotentialField pf = realise(field, rods, plan, spec, o.dz, thread_count(o.threads, 1 << 20));
   // timed like sweep.cpp:56,140-141 (BoundPotential, UTable and the row pool);
@@ -249,7 +255,7 @@ Rows solve_rows(const RefField& field, const mb::RodSet& rods, double gamma, con
   const mb::BoundPotential bound(pf, rods);
   const long rows = grid.rows();
   const int n = rods.size();
-  const mb::NodeSchedule sched = mb::schedule_for(spec);
+  const mb::NodeSchedule sched = spec ? mb::schedule_for(*spec) : mb::midpoint_schedule();
   std::unique_ptr<mb::UTable> table;
   if (rows > 1 && mb::UTable::bytes_estimate(n, plan.count, sched) <= o.table_budget_bytes)
     table = std::make_unique<mb::UTable>(bound, mb::StepWindow::of_plan(plan), sched);
@@ -269,9 +275,11 @@ Rows solve_rows(const RefField& field, const mb::RodSet& rods, double gamma, con
     const mb::GammaMatrix gm = mb::GammaMatrix::build(rods, beam);
     mb::ComplexMatrix R_init;
     if (bound.bulk_period())
-      R_init = mb::compute_bulk_reflection_proposed(bound, gm, o.dz, spec, popts, mb::BulkOptions{});
+      R_init = spec ? mb::compute_bulk_reflection_proposed(bound, gm, o.dz, *spec, popts, mb::BulkOptions{})
+                    : mb::compute_bulk_reflection_conventional(bound, gm, o.dz, mb::BulkOptions{});
     mb::SolveStats stats;
-    const mb::ComplexVector rho0 = mb::solve_proposed(bound, gm, plan, spec, popts, R_init, table.get(), &stats);
+    const mb::ComplexVector rho0 = spec ? mb::solve_proposed(bound, gm, plan, *spec, popts, R_init, table.get(), &stats)
+                                        : mb::solve_conventional(bound, gm, plan, R_init, table.get()).rho0;
     const mb::RealVector eta = mb::intensity(rho0, gm);
     for (int i = 0; i < n; ++i) {
       out.eta[(std::size_t)(row * n + i)] = eta(i);
@@ -426,6 +434,22 @@ PYBIND11_MODULE(mb_ref, m) {
           },
           py::arg("z_bottom"), py::arg("layers"), py::arg("bulk_period") = py::none())
       .def_static(
+          "tabulated",
+          [](double zb, std::vector<double> grid, std::vector<std::pair<std::pair<int, int>, std::vector<cd>>> entries,
+             py::object period) {
+            std::vector<mb::TabulatedEntry> es;
+            for (auto& e : entries) {
+              mb::TabulatedEntry t;
+              t.dm = Eigen::Vector2i(e.first.first, e.first.second);
+              t.values = e.second;
+              es.push_back(std::move(t));
+            }
+            std::optional<double> p;
+            if (!period.is_none()) p = period.cast<double>();
+            return RefField{mb::PotentialField::tabulated(zb, std::move(grid), std::move(es), p), {}, zb, p};
+          },
+          py::arg("z_bottom"), py::arg("z_grid"), py::arg("entries"), py::arg("bulk_period") = py::none())
+      .def_static(
           "atoms",
           [](double zb, py::array_t<double, py::array::forcecast> xyz, py::array_t<int, py::array::forcecast> species,
              py::array_t<double, py::array::forcecast> B, py::array_t<double, py::array::forcecast> ff_a,
@@ -510,7 +534,7 @@ PYBIND11_MODULE(mb_ref, m) {
     double secs = 0.0;
     {
       py::gil_scoped_release nogil;
-      const mb::StepperSpec& spec = spec_of(o);
+      const mb::StepperSpec* spec = spec_of(o);
       const mb::SlicingPlan plan = plan_of(f, o);
       const mb::PotentialField pf = realise(f, rods, plan, spec, o.dz, thread_count(o.threads, 1 << 20));
       mb::SweepOptions so;

@@ -358,7 +358,7 @@ class PotentialField:
 # ----------------------------------------------------------------- stepper
 class StepperSpec:
     """One-step integrator (proposed.hpp:23-43)."""
-    RK4, SPLITTING = 0, 1
+    RK4, SPLITTING, CONVENTIONAL = 0, 1, 2
     ABA, BAB = 0, 1
 
     def __init__(self, name, algorithm, variant=1, drift=(), kick=()):
@@ -370,8 +370,8 @@ class StepperSpec:
     def by_name(name):
         s = _Stepper()
         _check(lib().mb_stepper_by_name(name.encode(), C.byref(s)))
-        if s.algorithm == StepperSpec.RK4:
-            return StepperSpec(name, StepperSpec.RK4)
+        if s.algorithm in (StepperSpec.RK4, StepperSpec.CONVENTIONAL):
+            return StepperSpec(name, s.algorithm)
         drift = np.ctypeslib.as_array(C.cast(s.drift, C.POINTER(C.c_double)), (s.ndrift,)).copy()
         kick = np.ctypeslib.as_array(C.cast(s.kick, C.POINTER(C.c_double)), (s.nkick,)).copy()
         return StepperSpec(name, StepperSpec.SPLITTING, s.variant, drift, kick)

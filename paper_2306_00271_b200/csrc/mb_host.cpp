@@ -197,7 +197,7 @@ const Tables& tables() {
 
 // proposed.cpp:36-60
 void validate_stepper(const mb_stepper& s) {
-  if (s.algorithm == MB_STEP_RK4) return;
+  if (s.algorithm == MB_STEP_RK4 || s.algorithm == MB_STEP_CONVENTIONAL) return;
   if (s.algorithm != MB_STEP_SPLITTING) fail(MB_ERR_CONFIG, "stepper: unknown algorithm");
   const int nd = s.ndrift, nk = s.nkick;
   const bool shape_ok = s.variant == MB_SPLIT_BAB ? (nk == nd + 1) : (nd == nk + 1);
@@ -240,6 +240,11 @@ struct Schedule {
 };
 Schedule make_schedule(const mb_stepper& s) {
   Schedule sc;
+  if (s.algorithm == MB_STEP_CONVENTIONAL) {  // midpoint_schedule (stages.cpp:8), conventional.cpp:56
+    sc.frac = {0.5};
+    sc.occ2node = {0};
+    return sc;
+  }
   if (s.algorithm == MB_STEP_RK4) {
     sc.frac = {0.0, 0.5, 1.0};
     sc.occ2node = {0, 1, 1, 2};  // RK4 stages: foot, mid, mid, top
@@ -419,6 +424,8 @@ struct mb_context {
 struct mb_plan {
   mb_context* ctx = nullptr;
   bool big = false;      // large-N batched path (mb_large.cu)
+  bool conv = false;     // conventional multi-slice method (mb_conventional.cu)
+  long conv_ctas = 0;
   bool cluster = false;  // cluster-resident path (mb_cluster.cu)
   mbx::BigParams bp{};
   int stride = 0;
@@ -500,13 +507,19 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
   // per pair (mb_cluster.cu) when its shared-memory footprint fits, else the
   // batched large-N path (state in HBM). Final choice after the box size below.
   if (n > 256) fail(MB_ERR_CONFIG, "device path supports at most 256 rods, got " + std::to_string(n));
-  int npad = mbx::propagate_supported(n, stepper->algorithm == MB_STEP_RK4);
+  const bool conv = stepper->algorithm == MB_STEP_CONVENTIONAL;
+  if (conv && n > 32) fail(MB_ERR_CONFIG, "conventional method on the device supports at most 32 rods");
+  if (conv && fields[0].has_bulk_period)
+    fail(MB_ERR_CONFIG, "conventional method on the device: bulk seeding is not supported");
+  int npad = conv ? 0 : mbx::propagate_supported(n, stepper->algorithm == MB_STEP_RK4);
+  if (conv && opts->path != 0) fail(MB_ERR_CONFIG, "conventional method: path must be 0");
   if (opts->path == 1 && !npad) fail(MB_ERR_CONFIG, "resident kernel does not cover this rod count / stepper");
   if (opts->path < 0 || opts->path > 4) fail(MB_ERR_ARG, "options: path must be 0..4");
   if (opts->path >= 2) npad = 0;
+  if (conv) npad = 2 * n;
   if (fields[0].has_bulk_period && opts->path == 2)
     fail(MB_ERR_CONFIG, "bulk seeding runs in the resident and cluster kernels only (path 0, 1, 3 or 4)");
-  bool big = npad == 0;
+  bool big = npad == 0 && !conv;
   if (big) npad = (n + 7) & ~7;
 
   // slicing (slicing.hpp:17-34) and node heights (stages.cpp:25-30)
@@ -611,6 +624,7 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
   // round 1): cluster wins for the 61-pair N=199 case, the batched path for
   // 4096 pairs at N=127/255.
   bool cluster = false;
+  if (conv) big = false;
   // bulk seeding (per-pair period loop until R settles) exists only in the
   // on-chip kernels, so it takes the cluster kernel at any batch size
   const bool want_cluster = opts->path == 3 || opts->path == 4;
@@ -768,6 +782,9 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
     if (p.rk4) {
       p.nocc = 4;
       for (int r = 0; r < 4; ++r) p.occ_node[r] = sc.occ2node[(std::size_t)r];
+    } else if (conv) {
+      p.nocc = 1;
+      p.occ_node[0] = 0;
     } else {
       p.nocc = stepper->nkick;
       for (int r = 0; r < stepper->nkick; ++r) {
@@ -805,6 +822,11 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
     p.prof = dev_alloc<unsigned long long>(pl, 12);
     pl->big = big;
     pl->cluster = cluster;
+    pl->conv = conv;
+    if (conv) {
+      pl->conv_ctas = mbx::conventional_ctas(npairs);
+      p.scratch = dev_alloc<double>(pl, mbx::conventional_scratch_doubles(pl->conv_ctas));
+    }
     pl->stride = (int)stride;
     // cluster kernel: A, B, panel rows (+ the saved Q slab of a bulk period)
     if (cluster) {
@@ -930,7 +952,9 @@ void execute_plan(mb_plan* pl, cudaStream_t st) {
   cuda_check(cudaEventRecord(pl->ev[1], st), "event");
   cuda_check(cudaMemsetAsync(pl->prop.prof, 0, 12 * sizeof(unsigned long long), st), "memset");
   int npad = 0;
-  if (pl->big)
+  if (pl->conv)
+    cuda_check(mbx::launch_conventional(pl->prop, pl->conv_ctas, st, &pl->launches), "conventional kernel launch");
+  else if (pl->big)
     execute_big(pl, st);
   else if (pl->cluster)
     cuda_check(mbx::launch_cluster(pl->prop, st, &pl->launches), "cluster propagation kernel launch");
@@ -956,6 +980,8 @@ void raise_first_failure(const std::vector<mbx::PointStatus>& stv) {
     if (stv[i].code == MB_POINT_BULK_READ)
       fail(MB_ERR_BREAKDOWN, "bulk reflection read: solve_right: singular or ill-conditioned system (pair " +
                                  std::to_string(i) + ", period " + std::to_string(stv[i].step) + ")");
+    if (stv[i].code == MB_POINT_RECURSION)
+      fail(MB_ERR_BREAKDOWN, "conventional recursion: singular, ill-conditioned or nonfinite reflection" + where);
     if (stv[i].code == MB_POINT_BULK_CONVERGENCE)
       fail(MB_ERR_CONVERGENCE, "bulk reflection did not settle within 10000 periods (pair " + std::to_string(i) + ")");
     fail(MB_ERR_BREAKDOWN, "reflection extraction: solve_right: singular or ill-conditioned system" + where);
@@ -1211,6 +1237,8 @@ int mb_stepper_by_name(const char* name, mb_stepper* out) {
       *out = mb_stepper{MB_STEP_SPLITTING, MB_SPLIT_BAB, 6, t.sp4_drift, 7, t.sp4_kick};
     } else if (s == "sp6") {
       *out = mb_stepper{MB_STEP_SPLITTING, MB_SPLIT_BAB, 11, t.sp6_drift, 12, t.sp6_kick};
+    } else if (s == "conventional") {
+      *out = mb_stepper{MB_STEP_CONVENTIONAL, MB_SPLIT_BAB, 0, nullptr, 0, nullptr};
     } else {
       fail(MB_ERR_CONFIG, "unknown stepper '" + s + "' (expected rk4, sp4 or sp6)");
     }

@@ -9,6 +9,7 @@
 namespace mbx {
 
 constexpr int kMaxOcc = 32;  // kick occurrences (or RK stages) per step
+constexpr int MB_POINT_RECURSION_CODE = 6;  // = MB_POINT_RECURSION (conventional method)
 
 // Point status on the device (mirrors mb_point_status)
 struct PointStatus {
@@ -145,6 +146,11 @@ cudaError_t big_launch_check(const BigParams& p, int step, int mq, int mp, cudaS
 // with scratch (msa, msb)
 cudaError_t big_launch_gj(const BigParams& p, int mode, int step, int mq, int mp, int msa, int msb, int mx2,
                           double h, cudaStream_t st, int* launches);
+
+// conventional multi-slice method (mb_conventional.cu), N <= 32
+size_t conventional_scratch_doubles(long ctas);
+long conventional_ctas(long npairs);
+cudaError_t launch_conventional(const PropagateParams& p, long ctas, cudaStream_t st, int* launches);
 
 // launchers (mb_kernels.cu)
 cudaError_t launch_potential(const PotentialParams& p, cudaStream_t st, int* launches);

@@ -27,8 +27,30 @@ def run(role, out, slices=None):
     from paper_2306_00271_b200 import configs
     w = configs.config3()
     t0 = time.time()
-    if role.startswith("dev"):
-        eta, rho, st = H.run_device(w, fsal=True)
+    if role == "refdevU":
+        # the reference propagating the DEVICE's K1 table (tabulated on the
+        # exact node heights): separates U-input sensitivity from propagation
+        import mb_ref
+        import paper_2306_00271_b200 as mb
+        rods = mb.RodSet.build_first(mb.Lattice2D(w.a1, w.a2), w.n_rods)
+        plan = mb.Plan(rods, configs.product_fields(w), w.gamma, [(0, w.theta0[0], 0.0)],
+                       mb.SweepOptions(method=w.method, slices=w.slices, dz=-w.z_bottom / w.slices))
+        plan.execute()
+        z, coef = plan.node_heights(), plan.coefficients(0)
+        plan.close()
+        order = np.argsort(z, kind="stable")
+        zs, keep = np.unique(z[order], return_index=True)
+        tab = coef[order][keep]
+        dm = mb_ref.RodSet.build_first(mb_ref.Lattice2D(w.a1, w.a2), w.n_rods).diff_m
+        f = mb_ref.PotentialField.tabulated(w.z_bottom, list(zs), [((int(a), int(b)), list(tab[:, d]))
+                                                                  for d, (a, b) in enumerate(dm)])
+        rr = mb_ref.RodSet.build_first(mb_ref.Lattice2D(w.a1, w.a2), w.n_rods)
+        o = mb_ref.SweepOptions()
+        o.method, o.slices, o.dz, o.threads = w.method, w.slices, -w.z_bottom / w.slices, 0
+        c = mb_ref.rocking_curve(f, rr, w.gamma, mb_ref.AngleGrid.validated(list(w.theta0), [0.0]), o)
+        eta, rho, rh = c.eta, c.rho, c.rhst
+    elif role.startswith("dev"):
+        eta, rho, st = H.run_device(w, fsal=role != "dev3m_nofsal")
         rh = st["rhst"]
     elif role.startswith("ref"):
         import mb_ref
@@ -45,6 +67,10 @@ def report(paths):
     import harness as H
     d = {str(np.load(p)["role"]): np.load(p) for p in paths}
     want = d["ref"]["eta"]
+    if "refdevU" in d and "dev3m" in d:
+        out["dev3m_vs_refdevU"] = {"curve_error": H.curve_err(d["dev3m"]["eta"], d["refdevU"]["eta"]),
+                                   "entry_rel_err_floor_1e-10": H.entry_rel_err(d["dev3m"]["eta"], d["refdevU"]["eta"], 1e-10),
+                                   "rhst_differs_at_angles": np.nonzero(d["dev3m"]["rhst"] != d["refdevU"]["rhst"])[0].tolist()}
     out = {"workload": "cfg3-manybeam-N199-sp6 (full: 61 angles, 1000 slices)", "against": "ref (oracle/_ref, threshold 1000)",
            "rows": {}}
     for k, v in d.items():
