@@ -67,12 +67,12 @@ def report(paths):
     import harness as H
     d = {str(np.load(p)["role"]): np.load(p) for p in paths}
     want = d["ref"]["eta"]
+    out = {"workload": "cfg3-manybeam-N199-sp6 (full: 61 angles, 1000 slices)", "against": "ref (oracle/_ref, threshold 1000)",
+           "rows": {}}
     if "refdevU" in d and "dev3m" in d:
         out["dev3m_vs_refdevU"] = {"curve_error": H.curve_err(d["dev3m"]["eta"], d["refdevU"]["eta"]),
                                    "entry_rel_err_floor_1e-10": H.entry_rel_err(d["dev3m"]["eta"], d["refdevU"]["eta"], 1e-10),
                                    "rhst_differs_at_angles": np.nonzero(d["dev3m"]["rhst"] != d["refdevU"]["rhst"])[0].tolist()}
-    out = {"workload": "cfg3-manybeam-N199-sp6 (full: 61 angles, 1000 slices)", "against": "ref (oracle/_ref, threshold 1000)",
-           "rows": {}}
     for k, v in d.items():
         if k == "ref":
             continue
