@@ -83,6 +83,22 @@ class RodSet {
  public:
   static RodSet build(const Lattice2D& lat, double cutoff) { return make(lat, cutoff, 0); }
   static RodSet build_first(const Lattice2D& lat, int n) { return make(lat, 0.0, n); }
+  // a rod set given as the reference's tables (rods.hpp:28-37): k[n][2],
+  // m[n][2], diff[ndiff][2], diff_m[ndiff][2], diff_index[n*n]
+  static RodSet from_tables(std::vector<double> k, std::vector<int> m, std::vector<double> diff,
+                            std::vector<int> diff_m, std::vector<int> diff_index) {
+    RodSet r;
+    r.n_ = (int)(k.size() / 2);
+    r.ndiff_ = (int)(diff.size() / 2);
+    if (m.size() != k.size() || diff_m.size() != diff.size() || diff_index.size() != (std::size_t)r.n_ * r.n_)
+      throw ConfigError("rods: inconsistent table sizes");
+    r.k_ = std::move(k);
+    r.m_ = std::move(m);
+    r.diff_ = std::move(diff);
+    r.diff_m_ = std::move(diff_m);
+    r.diff_index_ = std::move(diff_index);
+    return r;
+  }
   int size() const { return n_; }
   int diff_count() const { return ndiff_; }
   Vec2 k(int i) const { return Vec2{k_[2 * i], k_[2 * i + 1]}; }

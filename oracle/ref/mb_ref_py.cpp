@@ -169,6 +169,10 @@ mb::PotentialField realise(const RefField& f, const mb::RodSet& rods, const mb::
     collect_nodes(mb::StepWindow::over(ze - p, ze, L), sched, zb);
     for (double z : zb) zs.push_back(map_z_bulk(z, ze, p));
   }
+  // the grid must cover [z_bottom, 0] (potential.cpp:68-69); midpoint
+  // schedules never touch the ends, so add them (exact nodes either way)
+  zs.push_back(f.z_bottom);
+  zs.push_back(0.0);
   std::sort(zs.begin(), zs.end());
   zs.erase(std::unique(zs.begin(), zs.end()), zs.end());
 

@@ -71,3 +71,13 @@ def test_cli_atoms_config_matches_api(tmp_path):
     out2 = tmp_path / "c0m.csv"
     assert subprocess.run([CLI, "simulate", "--config", str(p2), "--out", str(out2)]).returncode == 0
     assert out.read_bytes() == out2.read_bytes()
+
+
+def test_reference_types_adapter(ref):
+    """include/manybeam_b200_ref.hpp: the reference's own PotentialField /
+    RodSet / AngleGrid / SweepOptions through manybeam::b200::rocking_curve,
+    against manybeam::rocking_curve (oracle/_ref/tests/adapter_b200)."""
+    exe = os.path.join(ROOT, "oracle", "_ref", "tests", "adapter_b200")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "0 failed" in r.stdout
