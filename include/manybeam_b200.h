@@ -222,7 +222,7 @@ int mb_plan_info(const mb_plan* plan, long* slots, int* ndiff, long* coef_bytes,
 /* per-CTA average SM cycles by kernel phase (table wait, GEMM, kick epilogue,
  * finite check, Gershgorin, RHST, surface solve, prologue) of the last
  * execute; all zero unless the library was built with MB_PROFILE */
-int mb_plan_profile(const mb_plan* plan, double* cycles12);
+int mb_plan_profile(const mb_plan* plan, double* cycles16);
 /* EXTENSION (parity hooks; no reference counterpart): host copies of what
  * mb_plan_create built, so tests can compare them with the reference.
  *   node heights z[slots] in coefficient-table slot order (stages.cpp:25-47;

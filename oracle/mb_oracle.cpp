@@ -7,6 +7,8 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
+#include <string>
 #include <exception>
 #include <limits>
 #include <map>
@@ -73,10 +75,66 @@ CMat mul(const CMat& A, const CMat& B) {
 
 // kernels.cpp:60-80. X A = B  <=>  A^T X^T = B^T; PartialPivLU of A^T with
 // abs-score pivoting (Eigen scalar_score_coeff_op = abs), first maximum wins.
+namespace {
+// STUDY ONLY (MB_ORACLE_SOLVE=gj in the environment; never the default): the
+// solve as Gauss-Jordan column elimination on [A; B] with the same pivot
+// choice (first maximum of |A(k, j)| over j >= k), the form the device
+// kernels use. Separates the elimination form's rounding from everything
+// else in accuracy studies (tools/cfg3_accuracy.py).
+bool study_gj() {
+  static const bool on = [] {
+    const char* e = std::getenv("MB_ORACLE_SOLVE");
+    return e && std::string(e) == "gj";
+  }();
+  return on;
+}
+
+CMat gauss_jordan_right(const CMat& B, CMat A) {
+  const int n = A.r, rhs = B.r;
+  CMat X = B;
+  for (int k = 0; k < n; ++k) {
+    int p = k;
+    double best = std::abs(A(k, k));
+    for (int j = k + 1; j < n; ++j) {
+      const double s = std::abs(A(k, j));
+      if (s > best) {
+        best = s;
+        p = j;
+      }
+    }
+    if (best == 0.0) throw SingularMatrixError("solve_right: exactly singular matrix (zero pivot)");
+    if (p != k) {
+      for (int i = 0; i < n; ++i) std::swap(A(i, k), A(i, p));
+      for (int i = 0; i < rhs; ++i) std::swap(X(i, k), X(i, p));
+    }
+    const cd inv = 1.0 / A(k, k);
+    for (int i = 0; i < n; ++i) A(i, k) *= inv;
+    for (int i = 0; i < rhs; ++i) X(i, k) *= inv;
+    for (int j = 0; j < n; ++j) {
+      if (j == k) continue;
+      const cd f = A(k, j);
+      for (int i = 0; i < n; ++i) A(i, j) -= f * A(i, k);
+      for (int i = 0; i < rhs; ++i) X(i, j) -= f * X(i, k);
+    }
+  }
+  return X;
+}
+}  // namespace
+
 CMat solve_right(const CMat& B, const CMat& A) {
   if (A.r != A.c) throw SolverError("solve_right: A must be square");
   if (B.c != A.r) throw SolverError("solve_right: dimension mismatch");
   if (!A.all_finite() || !B.all_finite()) throw SolverError("solve_right: nonfinite input");
+  if (study_gj()) {
+    CMat X = gauss_jordan_right(B, A);
+    CMat XA = mul(X, A);
+    for (std::size_t i = 0; i < XA.a.size(); ++i) XA.a[i] -= B.a[i];
+    const double bnorm = B.norm();
+    const double resid = XA.norm() / (bnorm > 0 ? bnorm : 1.0);
+    if (!(resid <= 1e-10) || !X.all_finite())
+      throw SingularMatrixError("solve_right: ill-conditioned system, relative residual " + std::to_string(resid));
+    return X;
+  }
   const int n = A.r;
   CMat M(n, n);
   for (int i = 0; i < n; ++i)

@@ -547,11 +547,11 @@ class Plan:
         return {"slots": s.value, "ndiff": d.value, "coef_bytes": b.value, "npad": npad.value, "h2d_bytes": h2d.value}
 
     PHASES = ("table_wait", "gemm", "kick_epilogue", "rhst_gj", "gershgorin", "rhst_other", "surface", "prologue",
-              "gj_rows_pre", "gj_pivot", "gj_rows_post", "gj_sync")
+              "gj_rows_pre", "gj_pivot", "gj_rows_post", "gj_sync", "slot12", "slot13", "slot14", "slot15")
 
     def profile(self):
         """per-CTA cycles by phase (MB_PROFILE builds only)."""
-        v = np.zeros(12)
+        v = np.zeros(16)
         _check(lib().mb_plan_profile(self._h, _ptr(v)))
         return dict(zip(self.PHASES, v.tolist()))
 

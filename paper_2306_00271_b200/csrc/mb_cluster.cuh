@@ -38,6 +38,10 @@
 
 namespace cg = cooperative_groups;
 
+// lambdas of the kernel body are always inlined: an out-of-line lambda reads
+// every capture through its closure on the stack (generic loads of shared data)
+#define MB_INL __attribute__((always_inline))
+
 // slab width at NP=128 for splitting steppers (rk4 and NP=256 use 16)
 #ifndef MB_SW128
 #define MB_SW128 32
@@ -204,6 +208,131 @@ __device__ __forceinline__ void slab_gemm(double (&acc)[C::MB][C::NB][4], const 
       }
 }
 
+// The same product for a warp whose first ML row blocks are live (ML known at
+// compile time: no per-block branch in the k loop) with the operands of
+// k-step k0 + 4 loaded while the DMMAs of k0 run (register double buffer; the
+// last prefetch re-reads the final k-step, a harmless in-bounds load).
+template <class C, int ML>
+__device__ __forceinline__ void slab_gemm_ml(double (&acc)[C::MB][C::NB][4], const double2* __restrict__ box,
+                                             const int* __restrict__ soff, const int (&raddr)[C::MB],
+                                             const double* __restrict__ Xr, const double* __restrict__ Xi,
+                                             int lane, int kmax) {
+  constexpr int NB = C::NB;
+  const int kl = lane & 3, cl = lane >> 2;
+  double t1[ML][NB][2], t2[ML][NB][2], t3[ML][NB][2];
+#ifdef MB_GEMM_4M
+  double t4[ML][NB][2];
+#endif
+#pragma unroll
+  for (int m = 0; m < ML; ++m)
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        t1[m][nb][e] = t2[m][nb][e] = t3[m][nb][e] = 0.0;
+#ifdef MB_GEMM_4M
+        t4[m][nb][e] = 0.0;
+#endif
+      }
+  double2 a[ML];
+  double br[NB], bi[NB];
+  auto load = [&](int k0) MB_INL {
+    const int k = k0 + kl;
+    const int offk = soff[k];
+#pragma unroll
+    for (int m = 0; m < ML; ++m) a[m] = raddr[m] >= 0 ? box[raddr[m] - offk] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) {
+      const int o = ss<C::SW>(k, nb * 8 + cl);
+      br[nb] = Xr[o];
+      bi[nb] = Xi[o];
+    }
+  };
+  load(0);
+  const int klast = kmax - 4;
+#pragma unroll 1
+  for (int k0 = 0; k0 < kmax; k0 += 4) {
+    double ar[ML], ai[ML], xr[NB], xi[NB];
+#pragma unroll
+    for (int m = 0; m < ML; ++m) {
+      ar[m] = a[m].x;
+      ai[m] = a[m].y;
+    }
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) {
+      xr[nb] = br[nb];
+      xi[nb] = bi[nb];
+    }
+    load(min(k0 + 4, klast));
+#ifdef MB_GEMM_4M
+#pragma unroll
+    for (int m = 0; m < ML; ++m)
+#pragma unroll
+      for (int nb = 0; nb < NB; ++nb) dmma(t1[m][nb][0], t1[m][nb][1], ar[m], xr[nb]);
+#pragma unroll
+    for (int m = 0; m < ML; ++m)
+#pragma unroll
+      for (int nb = 0; nb < NB; ++nb) dmma(t2[m][nb][0], t2[m][nb][1], ai[m], xi[nb]);
+#pragma unroll
+    for (int m = 0; m < ML; ++m)
+#pragma unroll
+      for (int nb = 0; nb < NB; ++nb) dmma(t3[m][nb][0], t3[m][nb][1], ar[m], xi[nb]);
+#pragma unroll
+    for (int m = 0; m < ML; ++m)
+#pragma unroll
+      for (int nb = 0; nb < NB; ++nb) dmma(t4[m][nb][0], t4[m][nb][1], ai[m], xr[nb]);
+#else
+    double as[ML], xs[NB];
+#pragma unroll
+    for (int m = 0; m < ML; ++m) as[m] = ar[m] + ai[m];
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) xs[nb] = xr[nb] + xi[nb];
+#pragma unroll
+    for (int m = 0; m < ML; ++m)
+#pragma unroll
+      for (int nb = 0; nb < NB; ++nb) dmma(t1[m][nb][0], t1[m][nb][1], ar[m], xr[nb]);
+#pragma unroll
+    for (int m = 0; m < ML; ++m)
+#pragma unroll
+      for (int nb = 0; nb < NB; ++nb) dmma(t2[m][nb][0], t2[m][nb][1], ai[m], xi[nb]);
+#pragma unroll
+    for (int m = 0; m < ML; ++m)
+#pragma unroll
+      for (int nb = 0; nb < NB; ++nb) dmma(t3[m][nb][0], t3[m][nb][1], as[m], xs[nb]);
+#endif
+  }
+#pragma unroll
+  for (int m = 0; m < ML; ++m)
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        acc[m][nb][e] = t1[m][nb][e] - t2[m][nb][e];
+#ifdef MB_GEMM_4M
+        acc[m][nb][2 + e] = t3[m][nb][e] + t4[m][nb][e];
+#else
+        acc[m][nb][2 + e] = (t3[m][nb][e] - t1[m][nb][e]) - t2[m][nb][e];
+#endif
+      }
+}
+
+// dispatch on the warp's live row-block count (warp-uniform, fixed per kernel)
+template <class C>
+__device__ __forceinline__ void slab_gemm2(double (&acc)[C::MB][C::NB][4], const double2* __restrict__ box,
+                                          const int* __restrict__ soff, const int (&raddr)[C::MB],
+                                          const double* __restrict__ Xr, const double* __restrict__ Xi, int ml,
+                                          int lane, int kmax) {
+  static_assert(C::MB <= 4, "live-block dispatch covers MB <= 4");
+  if (C::MB >= 4 && ml == 4)
+    slab_gemm_ml<C, (C::MB >= 4 ? 4 : 1)>(acc, box, soff, raddr, Xr, Xi, lane, kmax);
+  else if (C::MB >= 3 && ml == 3)
+    slab_gemm_ml<C, (C::MB >= 3 ? 3 : 1)>(acc, box, soff, raddr, Xr, Xi, lane, kmax);
+  else if (ml == 2)
+    slab_gemm_ml<C, 2>(acc, box, soff, raddr, Xr, Xi, lane, kmax);
+  else if (ml == 1)
+    slab_gemm_ml<C, 1>(acc, box, soff, raddr, Xr, Xi, lane, kmax);
+}
+
 // residual tile configuration (SW rows x NP/8 columns per warp)
 template <int NP_, int SW_>
 struct RCfg {
@@ -254,7 +383,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = p.n;
 #ifdef MB_PROFILE
-  long long prof_t = clock64(), prof_acc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long prof_t = clock64(), prof_acc[kProfSlots] = {};
 #endif
 
   extern __shared__ __align__(16) unsigned char smem[];
@@ -298,7 +427,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
   // group barrier and peer reads (cluster: barrier.cluster / DSMEM; COOP:
   // counter barrier / L2)
   unsigned bar_gen = 0;  // barriers passed (thread 0; monotone over the pairs)
-  auto gsync = [&]() {
+  auto gsync = [&]() MB_INL {
     if constexpr (COOP) {
       __syncthreads();
       if (tid == 0) {
@@ -323,13 +452,13 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
       cg::this_cluster().sync();
     }
   };
-  auto peer = [&](auto* ptr, int r) {
+  auto peer = [&](auto* ptr, int r) MB_INL {
     if constexpr (COOP)
       return reinterpret_cast<decltype(ptr)>(reinterpret_cast<uintptr_t>(ptr) + (r - crank) * PUBB);
     else
       return cg::this_cluster().map_shared_rank(ptr, r);
   };
-  auto pld = [&](const auto* ptr) {
+  auto pld = [&](const auto* ptr) MB_INL {
     if constexpr (COOP)
       return __ldcg(ptr);
     else
@@ -382,10 +511,13 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
 
   // own elements: block m -> rows 8 (warp + 8 m) + lane/4, block nb -> slab
   // columns 8 nb + 2 (lane & 3) + {0, 1}
-  auto orow = [&](int m) { return 8 * (warp + 8 * m) + (lane >> 2); };
-  auto ocol = [&](int nb) { return 8 * nb + 2 * (lane & 3); };
-  auto live = [&](int m) { return 8 * (warp + 8 * m) < n; };
-  auto ld = [&](const double* Xr, const double* Xi, int m, int nb, double (&v)[4]) {
+  auto orow = [&](int m) MB_INL { return 8 * (warp + 8 * m) + (lane >> 2); };
+  auto ocol = [&](int nb) MB_INL { return 8 * nb + 2 * (lane & 3); };
+  auto live = [&](int m) MB_INL { return 8 * (warp + 8 * m) < n; };
+  int ml = 0;  // live row blocks of this warp (blocks m < ml)
+#pragma unroll
+  for (int m = 0; m < MB; ++m) ml += live(m) ? 1 : 0;
+  auto ld = [&](const double* Xr, const double* Xi, int m, int nb, double (&v)[4]) MB_INL {
     const int o = ss<SW>(orow(m), ocol(nb));
     const double2 a = *reinterpret_cast<const double2*>(Xr + o);
     const double2 b = *reinterpret_cast<const double2*>(Xi + o);
@@ -394,7 +526,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
     v[2] = b.x;
     v[3] = b.y;
   };
-  auto st = [&](double* Xr, double* Xi, int m, int nb, const double (&v)[4]) {
+  auto st = [&](double* Xr, double* Xi, int m, int nb, const double (&v)[4]) MB_INL {
     const int o = ss<SW>(orow(m), ocol(nb));
     *reinterpret_cast<double2*>(Xr + o) = make_double2(v[0], v[1]);
     *reinterpret_cast<double2*>(Xi + o) = make_double2(v[2], v[3]);
@@ -407,7 +539,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
   double* Nr = X1r;
   double* Ni = X1i;
   // initial_state (proposed.cpp:123-128): Q = diag(ginv)/2, P = (i/2) I
-  auto set_q_diag = [&](double* Xr, double* Xi, bool ginv_half) {
+  auto set_q_diag = [&](double* Xr, double* Xi, bool ginv_half) MB_INL {
     for (int w = tid; w < PL; w += CNT) {
       Xr[w] = 0.0;
       Xi[w] = 0.0;
@@ -443,13 +575,13 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
   // the propagation window: the slab (main) or one bulk period (bulk seeding,
   // proposed.cpp:311-321: the same stepper on the bulk window's step)
   bool bulk_phase = BULK && p.bulk_steps > 0;
-  auto wbase = [&]() -> long { return (BULK && bulk_phase) ? p.bulk_base : 0L; };
-  auto wkick = [&](int r) -> double { return (BULK && bulk_phase) ? bkick[r] : okick[r]; };
-  auto wdrift = [&](int r) -> double { return (BULK && bulk_phase) ? bdrift[r] : odrift[r]; };
-  auto slot_of = [&](int step, int r) -> long { return wbase() + (long)step * p.slot_stride + onode[r]; };
+  auto wbase = [&]() MB_INL -> long { return (BULK && bulk_phase) ? p.bulk_base : 0L; };
+  auto wkick = [&](int r) MB_INL -> double { return (BULK && bulk_phase) ? bkick[r] : okick[r]; };
+  auto wdrift = [&](int r) MB_INL -> double { return (BULK && bulk_phase) ? bdrift[r] : odrift[r]; };
+  auto slot_of = [&](int step, int r) MB_INL -> long { return wbase() + (long)step * p.slot_stride + onode[r]; };
   // TMA staging of one node's box: thread 0 arms the buffer's mbarrier and
   // issues a single cp.async.bulk; every thread waits on the phase
-  auto issue = [&](double2* dst, long slot) {
+  auto issue = [&](double2* dst, long slot) MB_INL {
     const int b = dst == boxes ? 0 : 1;
     if (tid == 0) {
       mbar_expect_tx(tfull + b, box_bytes);
@@ -457,7 +589,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
     }
     tpend |= 1u << b;
   };
-  auto wait_box = [&](double2* buf) {
+  auto wait_box = [&](double2* buf) MB_INL {
     const int b = buf == boxes ? 0 : 1;
     if ((tpend >> b) & 1u) {
       mbar_wait(tfull + b, (tph >> b) & 1u);
@@ -476,7 +608,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
   int L = p.nsteps;
   const bool fsal = !RK4 && p.fsal && p.variant == 1;
 
-  auto begin_occ = [&](int nstep, int nr) -> double2* {
+  auto begin_occ = [&](int nstep, int nr) MB_INL -> double2* {
     CPROF(2);
     wait_box(cur);
     __syncthreads();  // every warp is done with nxt (its previous box)
@@ -487,7 +619,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
     }
     return cur;
   };
-  auto end_occ = [&](int nstep, int nr) {
+  auto end_occ = [&](int nstep, int nr) MB_INL {
     if (nstep < L) {
       const long ns = slot_of(nstep, nr);
       if (ns != cur_slot) {
@@ -498,7 +630,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
       }
     }
   };
-  auto drift_swap = [&](double c) {
+  auto drift_swap = [&](double c) MB_INL {
     FOR_OWN {  // every block, padding rows included: they must stay exactly zero
       double q0[4];
       ld(Ar, Ai, m, nb, q0);
@@ -534,7 +666,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
   // resident kernel: warp 0 updates row k+1 and computes its pivot while the
   // other warps update the remaining panel rows; one CTA barrier per step).
   // Publishes the pivot table and raises the CTA's panel flag to `sid`.
-  auto factor_panel = [&](int sid) {
+  auto factor_panel = [&](int sid) MB_INL {
     const int kend = min(n, col0 + SW), nk = kend - col0;
     int* ptp = reinterpret_cast<int*>(tpub + 2 * SW);     // [16] pivot columns
     double2* ptinv = tpub;                                // [16] 1/pivot
@@ -576,6 +708,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
       }
       __syncthreads();
     }
+    CPROF(8);
     // publish the panel rows (F) to L2 for the consumers
     for (int w = tid; w < nk * (NP / 2); w += CNT) {
       const int lr = w / (NP / 2), j = 2 * (w % (NP / 2));
@@ -589,8 +722,9 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
       __threadfence();  // tables and rows visible cluster-wide before the flag
       *reinterpret_cast<volatile int*>(tpub + 3 * SW) = sid;
     }
+    CPROF(14);
   };
-  auto wait_panel = [&](int b, int sid) {
+  auto wait_panel = [&](int b, int sid) MB_INL {
     if (tid == 0) {
       int v;
       if constexpr (COOP) {
@@ -613,12 +747,9 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
     }
     __syncthreads();
   };
-  auto solve_blocked = [&]() -> bool {
+  auto solve_blocked = [&]() MB_INL -> bool {
     const int npan = (n + SW - 1) / SW;
     const int sid = ++solve_id;
-    CPROF(11);
-    if (crank == 0) factor_panel(sid);
-    CPROF(8);
     int* scol = reinterpret_cast<int*>(tloc);                   // [32] special columns
     int* pslot = scol + 2 * SW;                                 // [16] slot of p_k
     unsigned* smask = reinterpret_cast<unsigned*>(pslot + SW);  // [NP/32] special-column bitmask
@@ -631,13 +762,126 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
     const int lr = tid / TPR, cg = tid % TPR, gi = col0 + lr;
     const int rbase = lane & ~(TPR - 1);
     bool okb = true;
-    for (int b = 0; b < npan; ++b) {
+    int p0 = 0, nk = 0;
+    const double* war = M2r;  // panel rows, row-major, ld NP
+    const double* wai = M2i;
+    // apply the panel's 16 ops to the own A rows (half 0) or B rows (half 1)
+    auto consume = [&](int half) MB_INL {
+      const bool isA = half == 0;
+      if (isA && col0 + SW <= p0 + SW) return;  // CTA-uniform: no A rows below the panel
+      double* Xr = isA ? Ar_ : Br_;
+      double* Xi = isA ? Ai_ : Bi_;
+      const bool act = gi < n && (isA ? gi >= p0 + SW : true);
+      // (A) sequential ops on the special columns
+      double2 val[SLOTS];
+#pragma unroll
+      for (int u = 0; u < SLOTS; ++u) {
+        const int j = scol[cg + TPR * u];
+        val[u] = (act && j >= 0) ? make_double2(Xr[sw<NP>(lr, j)], Xi[sw<NP>(lr, j)]) : make_double2(0.0, 0.0);
+      }
+      double2 xk[SW];
+#pragma unroll
+      for (int lk = 0; lk < SW; ++lk) {
+        xk[lk] = make_double2(0.0, 0.0);
+        if (lk < nk) {
+          const int ps = pslot[lk], ks = lk;
+          auto pick = [&](int sl) MB_INL {
+            double2 v = val[0];
+#pragma unroll
+            for (int u = 1; u < SLOTS; ++u)
+              if (sl / TPR == u) v = val[u];
+            return make_double2(__shfl_sync(0xffffffffu, v.x, rbase | (sl % TPR)),
+                                __shfl_sync(0xffffffffu, v.y, rbase | (sl % TPR)));
+          };
+          const double2 xp = pick(ps);
+          const double2 xold = pick(ks);
+          const double2 x = cmul(xp, linv[lk]);
+          xk[lk] = x;
+#pragma unroll
+          for (int u = 0; u < SLOTS; ++u) {
+            const int sl = cg + TPR * u;
+            const double2 f = fs[lk * 2 * SW + sl];
+            const double2 v = (sl == ps) ? xold : val[u];
+            const double2 nv = make_double2(v.x - (f.x * x.x - f.y * x.y), v.y - (f.x * x.y + f.y * x.x));
+            val[u] = (sl == ks) ? x : nv;
+          }
+        }
+      }
+      if (act) {
+#pragma unroll
+        for (int u = 0; u < SLOTS; ++u) {
+          const int j = scol[cg + TPR * u];
+          if (j >= 0) {
+            Xr[sw<NP>(lr, j)] = val[u].x;
+            Xi[sw<NP>(lr, j)] = val[u].y;
+          }
+        }
+      }
+      // (B) other columns: X[i][j] -= sum_k x_k F_k[j] (F_k[j] = A[k][j]),
+      // F chunks from the owner through DSMEM, next chunk prefetched into
+      // registers while the current one is applied
+      // SW x WCH chunk, FR double2 per thread and plane
+      constexpr int FR = SW * (WCH / 2) / CNT;
+      auto fetch = [&](int j0, double2 (&a)[FR], double2 (&c)[FR]) MB_INL {
+#pragma unroll
+        for (int f = 0; f < FR; ++f) {
+          const int w = tid + f * CNT, ldt = w / (WCH / 2), j = j0 + 2 * (w % (WCH / 2));
+          a[f] = make_double2(0.0, 0.0);
+          c[f] = a[f];
+          if (ldt < nk && j < NP) {
+            const long o = (long)ldt * NP + j;
+            a[f] = __ldcg(reinterpret_cast<const double2*>(war + o));
+            c[f] = __ldcg(reinterpret_cast<const double2*>(wai + o));
+          }
+          if (j >= n || ((smask[j >> 5] >> (j & 31)) & 1u)) a[f].x = c[f].x = 0.0;
+          if (j + 1 >= n || ((smask[(j + 1) >> 5] >> ((j + 1) & 31)) & 1u)) a[f].y = c[f].y = 0.0;
+        }
+      };
+      double2 na[FR], nc[FR];
+      fetch(0, na, nc);
+      for (int j0 = 0; j0 < n; j0 += WCH) {
+        __syncthreads();  // previous chunk consumed (and the special write-back done)
+#pragma unroll
+        for (int f = 0; f < FR; ++f) {
+          const int w = tid + f * CNT, ldt = w / (WCH / 2), ldj = 2 * (w % (WCH / 2));
+          *reinterpret_cast<double2*>(wchr + ldt * WCH + ldj) = na[f];
+          *reinterpret_cast<double2*>(wchi + ldt * WCH + ldj) = nc[f];
+        }
+        __syncthreads();
+        if (j0 + WCH < n) fetch(j0 + WCH, na, nc);
+        if (act) {
+#pragma unroll
+          for (int u = 0; u < WCH / TPR; ++u) {
+            const int jj = cg + TPR * u, j = j0 + jj;
+            if (j >= n) continue;
+            const int o = sw<NP>(lr, j);
+            double xr = Xr[o], xi = Xi[o];
+#pragma unroll
+            for (int t = 0; t < SW; ++t) {
+              const double wr = wchr[t * WCH + jj], wi = wchi[t * WCH + jj];
+              xr -= xk[t].x * wr - xk[t].y * wi;
+              xi -= xk[t].x * wi + xk[t].y * wr;
+            }
+            Xr[o] = xr;
+            Xi[o] = xi;
+          }
+        }
+      }
+      __syncthreads();
+    };
+    // b = -1: CTA 0 factorises panel 0. Then, per panel b, every CTA applies
+    // its ops to the own A rows, CTA b + 1 factorises the next panel, and the
+    // B rows follow. One call site keeps factor_panel inlined (a second one
+    // made it an out-of-line call reading every capture through the stack).
+    for (int b = -1; b < npan; ++b) {
+      if (b >= 0) {
       wait_panel(b, sid);
       CPROF(9);
-      const int p0 = b * SW, nk = min(SW, n - p0);
+      p0 = b * SW;
+      nk = min(SW, n - p0);
       const double2* rt = peer(tpub, b);
-      const double* war = M2r + (long)p0 * NP;  // panel rows, row-major, ld NP
-      const double* wai = M2i + (long)p0 * NP;
+      war = M2r + (long)p0 * NP;
+      wai = M2i + (long)p0 * NP;
       if (tid < SW) {
         linv[tid] = pld(rt + tid);
         lpp[tid] = pld(reinterpret_cast<const int*>(rt + 2 * SW) + tid);
@@ -689,115 +933,12 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
       }
       __syncthreads();
       CPROF(10);
-      // apply the panel's 16 ops to the own A rows (half 0) or B rows (half 1)
-      auto consume = [&](int half) {
-        const bool isA = half == 0;
-        if (isA && col0 + SW <= p0 + SW) return;  // CTA-uniform: no A rows below the panel
-        double* Xr = isA ? Ar_ : Br_;
-        double* Xi = isA ? Ai_ : Bi_;
-        const bool act = gi < n && (isA ? gi >= p0 + SW : true);
-        // (A) sequential ops on the special columns
-        double2 val[SLOTS];
-#pragma unroll
-        for (int u = 0; u < SLOTS; ++u) {
-          const int j = scol[cg + TPR * u];
-          val[u] = (act && j >= 0) ? make_double2(Xr[sw<NP>(lr, j)], Xi[sw<NP>(lr, j)]) : make_double2(0.0, 0.0);
-        }
-        double2 xk[SW];
-#pragma unroll
-        for (int lk = 0; lk < SW; ++lk) {
-          xk[lk] = make_double2(0.0, 0.0);
-          if (lk < nk) {
-            const int ps = pslot[lk], ks = lk;
-            auto pick = [&](int sl) {
-              double2 v = val[0];
-#pragma unroll
-              for (int u = 1; u < SLOTS; ++u)
-                if (sl / TPR == u) v = val[u];
-              return make_double2(__shfl_sync(0xffffffffu, v.x, rbase | (sl % TPR)),
-                                  __shfl_sync(0xffffffffu, v.y, rbase | (sl % TPR)));
-            };
-            const double2 xp = pick(ps);
-            const double2 xold = pick(ks);
-            const double2 x = cmul(xp, linv[lk]);
-            xk[lk] = x;
-#pragma unroll
-            for (int u = 0; u < SLOTS; ++u) {
-              const int sl = cg + TPR * u;
-              const double2 f = fs[lk * 2 * SW + sl];
-              const double2 v = (sl == ps) ? xold : val[u];
-              const double2 nv = make_double2(v.x - (f.x * x.x - f.y * x.y), v.y - (f.x * x.y + f.y * x.x));
-              val[u] = (sl == ks) ? x : nv;
-            }
-          }
-        }
-        if (act) {
-#pragma unroll
-          for (int u = 0; u < SLOTS; ++u) {
-            const int j = scol[cg + TPR * u];
-            if (j >= 0) {
-              Xr[sw<NP>(lr, j)] = val[u].x;
-              Xi[sw<NP>(lr, j)] = val[u].y;
-            }
-          }
-        }
-        // (B) other columns: X[i][j] -= sum_k x_k F_k[j] (F_k[j] = A[k][j]),
-        // F chunks from the owner through DSMEM, next chunk prefetched into
-        // registers while the current one is applied
-        // SW x WCH chunk, FR double2 per thread and plane
-        constexpr int FR = SW * (WCH / 2) / CNT;
-        auto fetch = [&](int j0, double2 (&a)[FR], double2 (&c)[FR]) {
-#pragma unroll
-          for (int f = 0; f < FR; ++f) {
-            const int w = tid + f * CNT, ldt = w / (WCH / 2), j = j0 + 2 * (w % (WCH / 2));
-            a[f] = make_double2(0.0, 0.0);
-            c[f] = a[f];
-            if (ldt < nk && j < NP) {
-              const long o = (long)ldt * NP + j;
-              a[f] = __ldcg(reinterpret_cast<const double2*>(war + o));
-              c[f] = __ldcg(reinterpret_cast<const double2*>(wai + o));
-            }
-            if (j >= n || ((smask[j >> 5] >> (j & 31)) & 1u)) a[f].x = c[f].x = 0.0;
-            if (j + 1 >= n || ((smask[(j + 1) >> 5] >> ((j + 1) & 31)) & 1u)) a[f].y = c[f].y = 0.0;
-          }
-        };
-        double2 na[FR], nc[FR];
-        fetch(0, na, nc);
-        for (int j0 = 0; j0 < n; j0 += WCH) {
-          __syncthreads();  // previous chunk consumed (and the special write-back done)
-#pragma unroll
-          for (int f = 0; f < FR; ++f) {
-            const int w = tid + f * CNT, ldt = w / (WCH / 2), ldj = 2 * (w % (WCH / 2));
-            *reinterpret_cast<double2*>(wchr + ldt * WCH + ldj) = na[f];
-            *reinterpret_cast<double2*>(wchi + ldt * WCH + ldj) = nc[f];
-          }
-          __syncthreads();
-          if (j0 + WCH < n) fetch(j0 + WCH, na, nc);
-          if (act) {
-#pragma unroll
-            for (int u = 0; u < WCH / TPR; ++u) {
-              const int jj = cg + TPR * u, j = j0 + jj;
-              if (j >= n) continue;
-              const int o = sw<NP>(lr, j);
-              double xr = Xr[o], xi = Xi[o];
-#pragma unroll
-              for (int t = 0; t < SW; ++t) {
-                const double wr = wchr[t * WCH + jj], wi = wchi[t * WCH + jj];
-                xr -= xk[t].x * wr - xk[t].y * wi;
-                xi -= xk[t].x * wi + xk[t].y * wr;
-              }
-              Xr[o] = xr;
-              Xi[o] = xi;
-            }
-          }
-        }
-        __syncthreads();
-      };
       consume(0);  // A rows first: the next owner's panel depends on them
       CPROF(11);
+      }
       if (crank == b + 1) factor_panel(sid);
       CPROF(8);
-      consume(1);
+      if (b >= 0) consume(1);
       CPROF(11);
     }
     // an owner's rows and table are immutable for the rest of the solve, so
@@ -807,10 +948,10 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
     return okb;
   };
 
-  auto cluster_solve = [&]() -> bool {
+  auto cluster_solve = [&]() MB_INL -> bool {
     CPROF(5);
     gsync();  // M0 / M1 slabs of every CTA are visible
-    CPROF(8);
+    CPROF(12);
     // own 16 rows of A and B (rows >= n and columns >= n are zero)
     for (int w = tid; w < SW * (NP / 2); w += CNT) {
       const int lr = w / (NP / 2), j = 2 * (w % (NP / 2));
@@ -831,7 +972,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
       *reinterpret_cast<double2*>(Bi_ + so) = bi;
     }
     __syncthreads();
-    CPROF(9);
+    CPROF(12);
     const bool ok = solve_blocked();
     if (!ok) return false;
     if (!p.residual_check) return true;
@@ -932,13 +1073,13 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
       F += pld(rv + 7);
     }
     gsync();  // pubv[5..7] free again
-    CPROF(10);
+    CPROF(13);
     const double bnorm = sqrt(Bn);
     return sqrt(Rn) / (bnorm > 0.0 ? bnorm : 1.0) <= 1e-10 && F == 0.0;
   };
 
   // write own slab elements of A (from the Q plane) and B (P registers) to M0/M1
-  auto write_slabs = [&](bool surface) {
+  auto write_slabs = [&](bool surface) MB_INL {
     FOR_OWN {
       const int r = orow(m);
       if (r >= n) continue;
@@ -1004,7 +1145,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
         st(Yr, Yi, m, nb, v);
       }
       double2* box = begin_occ(step, 1);
-      slab_gemm<C>(acc, box, soff, raddr, Qr, Qi, warp, lane, kmax, n);
+      slab_gemm2<C>(acc, box, soff, raddr, Qr, Qi, ml, lane, kmax);
       CPROF(1);
       end_occ(step, 1);
       FOR_OWN {
@@ -1034,7 +1175,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
         st(Qr, Qi, m, nb, q0);
       }
       box = begin_occ(step, 2);
-      slab_gemm<C>(acc, box, soff, raddr, Yr, Yi, warp, lane, kmax, n);
+      slab_gemm2<C>(acc, box, soff, raddr, Yr, Yi, ml, lane, kmax);
       CPROF(1);
       end_occ(step, 2);
       FOR_OWN {
@@ -1065,7 +1206,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
         st(Qr, Qi, m, nb, qb);
       }
       box = begin_occ(step, 3);
-      slab_gemm<C>(acc, box, soff, raddr, Zr, Zi, warp, lane, kmax, n);
+      slab_gemm2<C>(acc, box, soff, raddr, Zr, Zi, ml, lane, kmax);
       CPROF(1);
       end_occ(step, 3);
       FOR_OWN {
@@ -1083,7 +1224,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
         st(Qr, Qi, m, nb, qb);
       }
       box = begin_occ(step + 1, 0);
-      slab_gemm<C>(acc, box, soff, raddr, Yr, Yi, warp, lane, kmax, n);
+      slab_gemm2<C>(acc, box, soff, raddr, Yr, Yi, ml, lane, kmax);
       CPROF(1);
       end_occ(step + 1, 0);
       FOR_OWN {
@@ -1109,7 +1250,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
         const int nr = last ? (fsal ? 1 : 0) : r + 1;
         if (p.variant == 0) drift_swap(wdrift(r));
         double2* box = begin_occ(nstep, nr);
-        slab_gemm<C>(acc, box, soff, raddr, Ar, Ai, warp, lane, kmax, n);
+        slab_gemm2<C>(acc, box, soff, raddr, Ar, Ai, ml, lane, kmax);
       CPROF(1);
         end_occ(nstep, nr);
         const double kc = (fsal && last && step + 1 < L) ? wfsal : wkick(r);
@@ -1278,7 +1419,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
         }
         __syncthreads();
         if (main) ++rhst;
-        CPROF(5);
+        CPROF(15);
       }
       CPROF(4);
     }
@@ -1420,7 +1561,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
   CPROF(6);
 #ifdef MB_PROFILE
   if (tid == 0 && p.prof)
-    for (int q = 0; q < 12; ++q) {
+    for (int q = 0; q < kProfSlots; ++q) {
       atomicAdd(p.prof + q, (unsigned long long)prof_acc[q]);
       prof_acc[q] = 0;
     }

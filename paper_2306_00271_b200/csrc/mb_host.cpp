@@ -819,7 +819,7 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
     p.eta = dev_alloc<double>(pl, (std::size_t)npairs * n);
     p.rho = dev_alloc<double2>(pl, (std::size_t)npairs * n);
     p.status = dev_alloc<mbx::PointStatus>(pl, (std::size_t)npairs);
-    p.prof = dev_alloc<unsigned long long>(pl, 12);
+    p.prof = dev_alloc<unsigned long long>(pl, mbx::kProfSlots);
     pl->big = big;
     pl->cluster = cluster;
     pl->conv = conv;
@@ -950,7 +950,7 @@ void execute_plan(mb_plan* pl, cudaStream_t st) {
   cuda_check(cudaEventRecord(pl->ev[0], st), "event");
   if (pl->use_k1) cuda_check(mbx::launch_potential(pl->pot, st, &pl->launches), "potential kernel launch");
   cuda_check(cudaEventRecord(pl->ev[1], st), "event");
-  cuda_check(cudaMemsetAsync(pl->prop.prof, 0, 12 * sizeof(unsigned long long), st), "memset");
+  cuda_check(cudaMemsetAsync(pl->prop.prof, 0, mbx::kProfSlots * sizeof(unsigned long long), st), "memset");
   int npad = 0;
   if (pl->conv)
     cuda_check(mbx::launch_conventional(pl->prop, pl->conv_ctas, st, &pl->launches), "conventional kernel launch");
@@ -1368,19 +1368,19 @@ int mb_plan_info(const mb_plan* plan, long* slots, int* ndiff, long* coef_bytes,
 int mb_plan_profile(const mb_plan* plan, double* cycles) {
   return guarded([&] {
     if (!plan || !cycles) fail(MB_ERR_ARG, "null argument");
-    double acc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    double acc[mbx::kProfSlots] = {};
     std::vector<const mb_plan*> parts;
     if (plan->shards.empty())
       parts.push_back(plan);
     else
       for (const mb_plan* sp : plan->shards) parts.push_back(sp);
     for (const mb_plan* sp : parts) {
-      unsigned long long v[12];
+      unsigned long long v[mbx::kProfSlots];
       cuda_check(cudaSetDevice(sp->ctx->device), "cudaSetDevice");
       cuda_check(cudaMemcpy(v, sp->prop.prof, sizeof v, cudaMemcpyDeviceToHost), "D2H profile");
-      for (int q = 0; q < 12; ++q) acc[q] += (double)v[q];
+      for (int q = 0; q < mbx::kProfSlots; ++q) acc[q] += (double)v[q];
     }
-    for (int q = 0; q < 12; ++q) cycles[q] = acc[q] / (double)plan->npairs;
+    for (int q = 0; q < mbx::kProfSlots; ++q) cycles[q] = acc[q] / (double)plan->npairs;
   });
 }
 

@@ -8,6 +8,7 @@
 
 namespace mbx {
 
+constexpr int kProfSlots = 16;  // MB_PROFILE phase slots
 constexpr int kMaxOcc = 32;  // kick occurrences (or RK stages) per step
 constexpr int MB_POINT_RECURSION_CODE = 6;  // = MB_POINT_RECURSION (conventional method)
 

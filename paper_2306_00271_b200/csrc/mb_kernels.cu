@@ -63,43 +63,56 @@ __global__ void potential_amp_kernel(const __grid_constant__ PotentialParams p) 
 }
 
 // coef[s][slot][boxpos[d]] = sum_t amp[s][t][d] * exp(-alpha_t (z_slot - zc_t)^2)
-// grid: (slot blocks of kSlotTile, S); threads over d. The z-Gaussians of the
-// slot tile are staged in shared memory; every amp element is read once per
-// tile and reused kSlotTile times from registers.
-constexpr int kSlotTile = 16;
+// grid: (structure x slot blocks of kSlotTile) folded into gridDim.x; threads
+// over d. The z-Gaussians of the slot tile are staged in shared memory in
+// chunks of kTermChunk terms (fixed 32 KB, any atom count); every amp element
+// is read once per tile and reused kSlotTile times from registers, the sums
+// stay in registers across chunks.
+constexpr int kSlotTile = 16, kTermChunk = 256;
 __global__ void __launch_bounds__(128) potential_coef_kernel(const __grid_constant__ PotentialParams p) {
-  extern __shared__ double zg[];  // [T][kSlotTile]
-  const int s = blockIdx.y;
-  const long slot0 = (long)blockIdx.x * kSlotTile;
+  __shared__ double zg[kTermChunk * kSlotTile];  // [t in chunk][kSlotTile]
+  const long tiles = (p.nslots + kSlotTile - 1) / kSlotTile;
+  const int s = (int)(blockIdx.x / tiles);
+  const long slot0 = (long)(blockIdx.x % tiles) * kSlotTile;
   const int nsl = (int)min((long)kSlotTile, p.nslots - slot0);
-  for (int i = threadIdx.x; i < p.T * kSlotTile; i += blockDim.x) {
-    const int t = i / kSlotTile, q = i % kSlotTile;
-    double v = 0.0;
-    if (q < nsl) {
-      const double dz = p.z_slot[slot0 + q] - p.term_zc[(long)s * p.T + t];
-      v = exp(-p.term_alpha[(long)s * p.T + t] * dz * dz);
-    }
-    zg[i] = v;
-  }
-  __syncthreads();
   const double2* amp = p.amp + (long)s * p.T * p.ndiff;
-  for (int d = threadIdx.x; d < p.ndiff; d += blockDim.x) {
+  // d loop outside so each thread keeps its sums across the term chunks
+  const int dlim = (p.ndiff + blockDim.x - 1) / blockDim.x * blockDim.x;
+  for (int d0 = 0; d0 < dlim; d0 += blockDim.x) {
+    const int d = d0 + threadIdx.x;
     double re[kSlotTile], im[kSlotTile];
 #pragma unroll
     for (int q = 0; q < kSlotTile; ++q) re[q] = im[q] = 0.0;
-    for (int t = 0; t < p.T; ++t) {
-      const double2 a = amp[(long)t * p.ndiff + d];
-#pragma unroll
-      for (int q = 0; q < kSlotTile; ++q) {
-        const double g = zg[t * kSlotTile + q];
-        re[q] = fma(a.x, g, re[q]);
-        im[q] = fma(a.y, g, im[q]);
+    for (int t0 = 0; t0 < p.T; t0 += kTermChunk) {
+      const int tn = min(kTermChunk, p.T - t0);
+      __syncthreads();
+      for (int i = threadIdx.x; i < tn * kSlotTile; i += blockDim.x) {
+        const int t = t0 + i / kSlotTile, q = i % kSlotTile;
+        double v = 0.0;
+        if (q < nsl) {
+          const double dz = p.z_slot[slot0 + q] - p.term_zc[(long)s * p.T + t];
+          v = exp(-p.term_alpha[(long)s * p.T + t] * dz * dz);
+        }
+        zg[i] = v;
       }
-    }
-    double2* out = p.coef + ((long)s * p.nslots + slot0) * p.box_size + p.boxpos[d];
+      __syncthreads();
+      if (d < p.ndiff)
+        for (int t = 0; t < tn; ++t) {
+          const double2 a = amp[(long)(t0 + t) * p.ndiff + d];
 #pragma unroll
-    for (int q = 0; q < kSlotTile; ++q)
-      if (q < nsl) out[(long)q * p.box_size] = make_double2(re[q], im[q]);
+          for (int q = 0; q < kSlotTile; ++q) {
+            const double g = zg[t * kSlotTile + q];
+            re[q] = fma(a.x, g, re[q]);
+            im[q] = fma(a.y, g, im[q]);
+          }
+        }
+    }
+    if (d < p.ndiff) {
+      double2* out = p.coef + ((long)s * p.nslots + slot0) * p.box_size + p.boxpos[d];
+#pragma unroll
+      for (int q = 0; q < kSlotTile; ++q)
+        if (q < nsl) out[(long)q * p.box_size] = make_double2(re[q], im[q]);
+    }
   }
 }
 
@@ -110,14 +123,9 @@ cudaError_t launch_potential(const PotentialParams& p, cudaStream_t st, int* lau
     potential_amp_kernel<<<blocks, 256, 0, st>>>(p);
     ++*launches;
   }
-  dim3 grid((unsigned)((p.nslots + kSlotTile - 1) / kSlotTile), (unsigned)p.S);
-  const size_t smem = (size_t)p.T * kSlotTile * sizeof(double);
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(potential_coef_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return e;
-  }
-  potential_coef_kernel<<<grid, 128, smem, st>>>(p);
+  const long blocks = (long)p.S * ((p.nslots + kSlotTile - 1) / kSlotTile);
+  if (blocks > 0x7fffffffL) return cudaErrorInvalidConfiguration;
+  potential_coef_kernel<<<(unsigned)blocks, 128, 0, st>>>(p);
   ++*launches;
   return cudaGetLastError();
 }
@@ -517,7 +525,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
   };
   const int kmax = (n + 3) & ~3;
 #ifdef MB_PROFILE
-  long long prof_t = clock64(), prof_acc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long prof_t = clock64(), prof_acc[kProfSlots] = {};
 #endif
 
   // current / next Q planes (pointer swap, never a runtime-indexed array)
@@ -1112,7 +1120,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
   PROF_MARK(6);
 #ifdef MB_PROFILE
   if (tid == 0 && p.prof)
-    for (int q = 0; q < 12; ++q) atomicAdd(p.prof + q, (unsigned long long)prof_acc[q]);
+    for (int q = 0; q < kProfSlots; ++q) atomicAdd(p.prof + q, (unsigned long long)prof_acc[q]);
 #endif
   if (tid == 0) {
     PointStatus st;

@@ -393,9 +393,13 @@ __device__ __forceinline__ void gj_pivot(const double2 (&a)[(C::NP + 31) / 32], 
     // 1/|pivot|^2: RCP64H seed + two Newton steps (inverse by multiplication,
     // like any reciprocal-scaled elimination; rounding-level only)
     double r;
+#ifdef MB_EXACT_RCP
+    r = 1.0 / best;  // accuracy study build: IEEE division
+#else
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(best));
     r = r * fma(-best, r, 2.0);
     r = r * fma(-best, r, 2.0);
+#endif
     sc.inv[slot] = best > 0.0 ? make_double2(akp.x * r, -akp.y * r) : make_double2(0.0, 0.0);
   }
 }

@@ -50,13 +50,20 @@ def run(role, out, slices=None):
         c = mb_ref.rocking_curve(f, rr, w.gamma, mb_ref.AngleGrid.validated(list(w.theta0), [0.0]), o)
         eta, rho, rh = c.eta, c.rho, c.rhst
     elif role.startswith("dev"):
-        eta, rho, st = H.run_device(w, fsal=role != "dev3m_nofsal")
+        # dev3m: auto path (cooperative groups at cfg3); devpath2 / devpath3:
+        # the batched and the thread-block-cluster designs on the same inputs
+        path = int(role[len("devpath"):]) if role.startswith("devpath") else 0
+        eta, rho, st = H.run_device(w, fsal=role != "dev3m_nofsal", path=path)
         rh = st["rhst"]
     elif role.startswith("ref"):
         import mb_ref
         thr = 1500.0 if role == "ref1500" else 1000.0
         eta, rho, rh = H.run_oracle(mb_ref, w, threads=0, threshold=thr)
     else:
+        # port: the restatement; portgj: the same with the study-only
+        # Gauss-Jordan solve (MB_ORACLE_SOLVE=gj), the device's elimination form
+        if role == "portgj":
+            os.environ["MB_ORACLE_SOLVE"] = "gj"
         import mb_oracle
         eta, rho, rh = H.run_oracle(mb_oracle, w, threads=0)
     np.savez_compressed(out, eta=eta, rho=rho, rhst=np.asarray(rh), role=role, seconds=time.time() - t0)
