@@ -607,6 +607,15 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
   const int nocc = p.nocc;
   int L = p.nsteps;
   const bool fsal = !RK4 && p.fsal && p.variant == 1;
+  // FSAL (BAB): the last kick of a step and the first kick of the next share
+  // the node height and Q, so they share ONE product W = (U + G^2) Q. Both
+  // subtractions run separately with the reference's rounding, after the
+  // end-of-step check: P1 = P - k_last W (checked), then P - k_first W if no
+  // RHST follows, else the RHST on (Q, P1) and the first kick against Q = I,
+  // W = U + G^2 read from the node's box (U I is exact in the reference).
+  // Bitwise the schedule of fsal = 0, one GEMM fewer per step.
+  double2* mbox = boxes;
+  bool qident = false;  // BAB without FSAL: this step's first kick sees Q = I (an RHST just ran)
 
   auto begin_occ = [&](int nstep, int nr) MB_INL -> double2* {
     CPROF(2);
@@ -635,7 +644,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
       double q0[4];
       ld(Ar, Ai, m, nb, q0);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) q0[q] += c * P[m][nb][q];
+      for (int q = 0; q < 4; ++q) q0[q] = drift_ref(q0[q], c, P[m][nb][q]);
       st(Nr, Ni, m, nb, q0);
     }
     double* t = Ar;
@@ -644,6 +653,24 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
     t = Ai;
     Ai = Ni;
     Ni = t;
+  };
+
+  // a kick against Q = I (right after an RHST): W = U + G^2 straight from the
+  // node's box, as the reference's U * I is exact (no 3M rounding of U)
+  auto ukick = [&](const double2* ubox, double kf) MB_INL {
+    FOR_OWN {
+      if (!live(m)) continue;
+      const int r = orow(m);
+      const double g2 = g2s[r];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = col0 + ocol(nb) + e;
+        double2 u = make_double2(0.0, 0.0);
+        if (r < n && c < n) u = ubox[raddr[m] - soff[c]];
+        P[m][nb][e] = kick_ref(P[m][nb][e], kf, u.x, g2, (r == c && r < n) ? 1.0 : 0.0);
+        P[m][nb][2 + e] = kick_ref(P[m][nb][2 + e], kf, u.y, g2, 0.0);
+      }
+    }
   };
 
   // ---------------------------------------------------------------- solve
@@ -700,6 +727,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
         gj_rows<C, 1>(Ar_, Ai_, Br_, Bi_, rows, isA, k, piv, inv, fj, row, lane);
         gj_pivot<C>(row[0], k + 1, n, fpub + (slot ^ 1) * NP, *sc, slot ^ 1, lane);
       }
+      CPROF(6);  // (thread 0 = warp 0: the pivot chain of the step)
       for (int lr = lk + 2 + (warp - 1); warp > 0 && lr < nk; lr += CNW - 1) {
         const int rows[1] = {lr};
         const bool isA[1] = {true};
@@ -817,6 +845,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
           }
         }
       }
+      CPROF(7);  // special columns
       // (B) other columns: X[i][j] -= sum_k x_k F_k[j] (F_k[j] = A[k][j]),
       // F chunks from the owner through DSMEM, next chunk prefetched into
       // registers while the current one is applied
@@ -1089,15 +1118,8 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
       double a[4], b[4];
       if (surface) {  // T = G Q - i P, R = G Q + i P
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const double qr = q0[e], qi = q0[2 + e];
-          const double gqr = g.x * qr - g.y * qi, gqi = g.x * qi + g.y * qr;
-          const double pr = P[m][nb][e], pi = P[m][nb][2 + e];
-          a[e] = gqr + pi;
-          a[2 + e] = gqi - pr;
-          b[e] = gqr - pi;
-          b[2 + e] = gqi + pr;
-        }
+        for (int e = 0; e < 2; ++e)
+          tau_rho_ref(g, q0[e], q0[2 + e], P[m][nb][e], P[m][nb][2 + e], a[e], a[2 + e], b[e], b[2 + e]);
       } else {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -1126,10 +1148,10 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
   L = (BULK && bulk_phase) ? p.bulk_steps : p.nsteps;
   const double wh = (BULK && bulk_phase) ? p.bulk_h : p.h;
   const double wfin = (BULK && bulk_phase) ? p.bulk_final_drift : p.final_drift;
-  const double wfsal = (BULK && bulk_phase) ? p.bulk_fsal_kick : p.fsal_kick;
   const int step_off = (int)(period * L);
   cur_slot = slot_of(0, 0);
   issue(cur, cur_slot);
+  qident = false;
   for (int step = 0; step < L; ++step) {
     if constexpr (RK4) {
       // classical RK4 (proposed.cpp:141-168) as in the resident kernel, with
@@ -1250,17 +1272,27 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
         const int nr = last ? (fsal ? 1 : 0) : r + 1;
         if (p.variant == 0) drift_swap(wdrift(r));
         double2* box = begin_occ(nstep, nr);
+        if (qident) {  // r == 0 right after an RHST: no product needed
+          ukick(box, wkick(r));
+          end_occ(nstep, nr);
+          qident = false;
+        } else {
         slab_gemm2<C>(acc, box, soff, raddr, Ar, Ai, ml, lane, kmax);
       CPROF(1);
         end_occ(nstep, nr);
-        const double kc = (fsal && last && step + 1 < L) ? wfsal : wkick(r);
-        FOR_OWN {
+        if (last) mbox = box;  // FSAL: node of the next step's first kick
+        const double kc = wkick(r);
+        FOR_OWN {  // acc <- W = U Q + G^2 Q (kept for an FSAL-merged next kick)
           if (!live(m)) continue;
           double q0[4];
           ld(Ar, Ai, m, nb, q0);
           const double g2 = g2s[orow(m)];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) P[m][nb][q] -= kc * (acc[m][nb][q] + g2 * q0[q]);
+          for (int q = 0; q < 4; ++q) {
+            acc[m][nb][q] = w_ref(acc[m][nb][q], g2, q0[q]);
+            P[m][nb][q] = sub_ref(P[m][nb][q], kc, acc[m][nb][q]);
+          }
+        }
         }
         if (p.variant == 1 && !last) drift_swap(wdrift(r));
       }
@@ -1368,6 +1400,14 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
         break;
       }
       const double xi = n == 0 ? 1.0 : (ND > 0.0 ? inf_d() : H / Lo);
+      if (fsal && step + 1 < L && !(xi > p.threshold)) {  // the next step's first kick, shared W
+        const double kf = wkick(0);
+        FOR_OWN {
+          if (!live(m)) continue;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) P[m][nb][q] = sub_ref(P[m][nb][q], kf, acc[m][nb][q]);
+        }
+      }
       if (xi > p.threshold) {
         // P <- P Q^-1, Q <- I (proposed.cpp:196-202)
         // the prefetched box of the next occurrence stays in flight into its buffer
@@ -1419,6 +1459,10 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
         }
         __syncthreads();
         if (main) ++rhst;
+        if (fsal && step + 1 < L)
+          ukick(mbox, wkick(0));  // the next step's first kick, Q = I
+        else
+          qident = !RK4 && p.variant == 1;  // BAB: the next step opens with a kick on Q = I
         CPROF(15);
       }
       CPROF(4);

@@ -85,6 +85,31 @@ __device__ __forceinline__ void mbar_wait_cluster(unsigned long long* bar, unsig
       : "memory");
 }
 
+// Splitting kick / drift with the reference's rounding (proposed.cpp:133-137,
+// 180-193): apply_w forms out = U X, then out += G^2 X (product, then sum),
+// then P -= (h b) out; a drift is Q += (h a) P. Each operation rounds once,
+// as the reference's Eigen expressions do on x86-64 without FMA; the _rn
+// intrinsics are never contracted into FMAs. The conditioning of deep slabs
+// (cfg3) amplifies a contracted epilogue's different rounding to ~5e-8 in eta.
+__device__ __forceinline__ double w_ref(double uq, double g2, double q) { return __dadd_rn(uq, __dmul_rn(g2, q)); }
+__device__ __forceinline__ double sub_ref(double p, double c, double w) { return __dsub_rn(p, __dmul_rn(c, w)); }
+__device__ __forceinline__ double kick_ref(double p, double c, double uq, double g2, double q) {
+  return sub_ref(p, c, w_ref(uq, g2, q));
+}
+__device__ __forceinline__ double drift_ref(double q, double c, double p) { return __dadd_rn(q, __dmul_rn(c, p)); }
+// to_tau_rho (proposed.cpp:108-113) with the reference's rounding:
+// G Q (complex product, two rounded products and one rounded sum per part),
+// T = G Q - i P, R = G Q + i P (i P = (-pi, pr) exactly).
+__device__ __forceinline__ void tau_rho_ref(double2 g, double qr, double qi, double pr, double pi, double& tr,
+                                            double& ti, double& rr, double& ri) {
+  const double gqr = __dsub_rn(__dmul_rn(g.x, qr), __dmul_rn(g.y, qi));
+  const double gqi = __dadd_rn(__dmul_rn(g.x, qi), __dmul_rn(g.y, qr));
+  tr = __dadd_rn(gqr, pi);
+  ti = __dsub_rn(gqi, pr);
+  rr = __dsub_rn(gqr, pi);
+  ri = __dadd_rn(gqi, pr);
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

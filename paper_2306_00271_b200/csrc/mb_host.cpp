@@ -915,7 +915,11 @@ void execute_big(mb_plan* pl, cudaStream_t st) {
   s = mbx::BigStage{0, 0, 0, 0, p.h, 0.0, 0.0, qc, -1, P, -1, -1, -1, -1, -1};
   launch(s);
   const int nk = p.nocc;
-  const bool fsal = p.fsal && p.variant == 1;
+  // FSAL is not merged on the batched path: a merged kick must keep the
+  // reference's two roundings around the end-of-step check (see the on-chip
+  // kernels), and here the shared product would be an extra N x N plane per
+  // pair in HBM. Unmerged kicks give exactly the fsal = 0 results.
+  const bool fsal = false;
   auto drift = [&](double c) {
     mbx::BigStage d{2, 0, 0, 0, 0.0, c, 0.0, qc, qc ^ 1, P, -1, -1, -1, -1, -1};
     launch(d);

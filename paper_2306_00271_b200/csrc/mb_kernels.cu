@@ -294,7 +294,7 @@ __device__ bool gauss_jordan_dominant(double* Ar, double* Ai, double* Br, double
           }
 #pragma unroll
         for (int t = 0; t < 8; ++t) {
-          if (t >= bsz) break;
+          if (t < bsz) {  // predicated, not break: R stays in registers
           const int k = k0 + t;
           double vmax = 0.0, vkk = 0.0;
           double2 rk = make_double2(0.0, 0.0);
@@ -320,7 +320,7 @@ __device__ bool gauss_jordan_dominant(double* Ar, double* Ai, double* Br, double
           const double2 inv = make_double2(rk.x * r, -rk.y * r);
 #pragma unroll
           for (int i = t + 1; i < 8; ++i) {
-            if (i >= bsz) break;
+            if (i < bsz) {
             double2 xi = R[i][0];
 #pragma unroll
             for (int q = 1; q < NQ; ++q)
@@ -335,6 +335,8 @@ __device__ bool gauss_jordan_dominant(double* Ar, double* Ai, double* Br, double
                   make_double2(R[i][q].x - (f.x * x.x - f.y * x.y), R[i][q].y - (f.x * x.y + f.y * x.x));
               R[i][q] = (j == k) ? x : nv;
             }
+            }
+          }
           }
         }
       }
@@ -517,7 +519,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
   const double2* coef = p.coef + (long)p.pair_struct[pair] * p.nslots * p.box_size;
   const int gtid = wm * 32 + lane;  // thread index inside the column group
   constexpr int GNT = C::NT / C::WN;
-  auto group_sync = [&]() {
+  auto group_sync = [&]() __attribute__((always_inline)) {
     if constexpr (C::WN == 1)
       __syncthreads();
     else
@@ -597,15 +599,14 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
   // (BULK = false: every window parameter is the slab's, read from the
   // parameter space; the bulk machinery compiles away)
   bool bulk_phase = BULK && p.bulk_steps > 0;
-  auto WL = [&]() -> int { return (BULK && bulk_phase) ? p.bulk_steps : p.nsteps; };
-  auto wbase = [&]() -> long { return (BULK && bulk_phase) ? p.bulk_base : 0L; };
-  auto wh = [&]() -> double { return (BULK && bulk_phase) ? p.bulk_h : p.h; };
-  auto wfin = [&]() -> double { return (BULK && bulk_phase) ? p.bulk_final_drift : p.final_drift; };
-  auto wfsal = [&]() -> double { return (BULK && bulk_phase) ? p.bulk_fsal_kick : p.fsal_kick; };
-  auto wkick = [&](int r) -> double { return (BULK && bulk_phase) ? bkick[r] : okick[r]; };
-  auto wdrift = [&](int r) -> double { return (BULK && bulk_phase) ? bdrift[r] : odrift[r]; };
+  auto WL = [&]() __attribute__((always_inline)) -> int { return (BULK && bulk_phase) ? p.bulk_steps : p.nsteps; };
+  auto wbase = [&]() __attribute__((always_inline)) -> long { return (BULK && bulk_phase) ? p.bulk_base : 0L; };
+  auto wh = [&]() __attribute__((always_inline)) -> double { return (BULK && bulk_phase) ? p.bulk_h : p.h; };
+  auto wfin = [&]() __attribute__((always_inline)) -> double { return (BULK && bulk_phase) ? p.bulk_final_drift : p.final_drift; };
+  auto wkick = [&](int r) __attribute__((always_inline)) -> double { return (BULK && bulk_phase) ? bkick[r] : okick[r]; };
+  auto wdrift = [&](int r) __attribute__((always_inline)) -> double { return (BULK && bulk_phase) ? bdrift[r] : odrift[r]; };
   // table pipeline: slot of occurrence (step, r) = base + step*stride + node
-  auto slot_of = [&](int step, int r) -> long { return wbase() + (long)step * p.slot_stride + onode[r]; };
+  auto slot_of = [&](int step, int r) __attribute__((always_inline)) -> long { return wbase() + (long)step * p.slot_stride + onode[r]; };
   // TMA staging: the group's first thread arms the buffer's mbarrier with the
   // byte count and issues one cp.async.bulk of the node's box; every thread
   // of the group waits on the phase before reading. pend / ph: per buffer,
@@ -614,7 +615,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
   unsigned long long* const barA = tbar + 2 * wn;
   const unsigned box_bytes = (unsigned)p.box_size * (unsigned)sizeof(double2);
   unsigned pend = 0u, ph = 0u;
-  auto issue = [&](double2* dst, long slot) {
+  auto issue = [&](double2* dst, long slot) __attribute__((always_inline)) {
     const int b = dst == bufA ? 0 : 1;
     if (gtid == 0) {
       mbar_expect_tx(barA + b, box_bytes);
@@ -622,7 +623,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
     }
     pend |= 1u << b;
   };
-  auto wait_box = [&](double2* buf) {
+  auto wait_box = [&](double2* buf) __attribute__((always_inline)) {
     const int b = buf == bufA ? 0 : 1;
     if ((pend >> b) & 1u) {
       mbar_wait(barA + b, (ph >> b) & 1u);
@@ -639,10 +640,19 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
   int code = 0, fail_step = 0;
   const int nocc = p.nocc;
   const bool fsal = !RK4 && p.fsal && p.variant == 1;
+  // FSAL (BAB): the last kick of a step and the first kick of the next share
+  // the node height and Q, hence one product W = (U + G^2) Q. Both
+  // subtractions run separately with the reference's rounding around the
+  // end-of-step check (P1 = P - k_last W is what the check and an RHST see);
+  // after an RHST the first kick uses Q = I, W = U + G^2 from the node's box
+  // (U I is exact in the reference). Bitwise the results of fsal = 0.
+  double2* mbox = bufA;
+  bool qident = false;  // BAB without FSAL: this step's first kick sees Q = I (an RHST just ran)
+
 
   // Barrier that publishes the previous phase's shared-memory writes and the
   // table of occurrence (step, r); prefetches the next occurrence's table.
-  auto begin_occ = [&](int nstep, int nr) -> double2* {
+  auto begin_occ = [&](int nstep, int nr) __attribute__((always_inline)) -> double2* {
     PROF_MARK(2);
     wait_box(cur);
     group_sync();  // every warp of the group is done with nxt (its previous box)
@@ -653,7 +663,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
     }
     return cur;
   };
-  auto end_occ = [&](int nstep, int nr) {
+  auto end_occ = [&](int nstep, int nr) __attribute__((always_inline)) {
     if (nstep < WL()) {
       const long ns = slot_of(nstep, nr);
       if (ns != cur_slot) {
@@ -668,12 +678,12 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
 #define FOR_BLK _Pragma("unroll") for (int mb = 0; mb < MB; ++mb) _Pragma("unroll") for (int nb = 0; nb < NB; ++nb)
   // splitting drift into the other Q buffer: Qn = Q + c P (own elements); no
   // write-after-read hazard with warps still reading Q in their GEMM.
-  auto drift_swap = [&](double c) {
+  auto drift_swap = [&](double c) __attribute__((always_inline)) {
     FOR_BLK {
       double q0[4];
       own.ld(Ar, Ai, mb, nb, q0);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) q0[q] += c * P[mb][nb][q];
+      for (int q = 0; q < 4; ++q) q0[q] = drift_ref(q0[q], c, P[mb][nb][q]);
       own.st(Nr, Ni, mb, nb, q0);
       if constexpr (XS)
         *reinterpret_cast<double2*>(Ns + sw<NP>(own.r(mb), own.c(nb))) = make_double2(q0[0] + q0[2], q0[1] + q0[3]);
@@ -688,8 +698,23 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
     As = Ns;
     Ns = t;
   };
-  // sum plane of the current Q (splitting); after the initial state and RHST
-  auto rebuild_sum = [&]() {
+  // a kick against Q = I (right after an RHST): W = U + G^2 straight from the
+  // node's box, as the reference's U * I is exact (no 3M rounding of U)
+  auto ukick = [&](const double2* ubox, double kf) __attribute__((always_inline)) {
+    FOR_BLK {
+      const int r = own.r(mb);
+      const double g2 = g2s[r];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = own.c(nb) + e;
+        double2 u = make_double2(0.0, 0.0);
+        if (r < n && c < n) u = ubox[raddr[mb] - soff[c]];
+        P[mb][nb][e] = kick_ref(P[mb][nb][e], kf, u.x, g2, (r == c && r < n) ? 1.0 : 0.0);
+        P[mb][nb][2 + e] = kick_ref(P[mb][nb][2 + e], kf, u.y, g2, 0.0);
+      }
+    }
+  };  // sum plane of the current Q (splitting); after the initial state and RHST
+  auto rebuild_sum = [&]() __attribute__((always_inline)) {
     if constexpr (XS)
       for (int w = tid; w < NP * NP; w += C::NT) As[w] = Ar[w] + Ai[w];
   };
@@ -712,6 +737,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
   const int step_off = (int)(period * L);
   cur_slot = slot_of(0, 0);
   issue(cur, cur_slot);
+  qident = false;
   for (int step = 0; step < L; ++step) {
     if constexpr (RK4) {
       // ---------------- classical RK4 (proposed.cpp:141-168), restructured:
@@ -865,16 +891,26 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
         const int nr = last ? (fsal ? 1 : 0) : r + 1;
         if (p.variant == 0) drift_swap(wdrift(r));  // ABA: drift before kick r
         double2* box = begin_occ(nstep, nr);
+        if (qident) {  // r == 0 right after an RHST: no product needed
+          ukick(box, wkick(r));
+          end_occ(nstep, nr);
+          qident = false;
+        } else {
         gemm_box<C, XS>(acc, box, soff, raddr, Ar, Ai, own.col0, lane, kmax, As);
         PROF_MARK(1);
         end_occ(nstep, nr);
-        const double kc = (fsal && last && step + 1 < L) ? wfsal() : wkick(r);
-        FOR_BLK {
+        if (last) mbox = box;  // FSAL: node of the next step's first kick
+        const double kc = wkick(r);
+        FOR_BLK {  // acc <- W = U Q + G^2 Q (kept for an FSAL-merged next kick)
           double q0[4];
           own.ld(Ar, Ai, mb, nb, q0);
           const double g2 = g2s[own.r(mb)];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) P[mb][nb][q] -= kc * (acc[mb][nb][q] + g2 * q0[q]);
+          for (int q = 0; q < 4; ++q) {
+            acc[mb][nb][q] = w_ref(acc[mb][nb][q], g2, q0[q]);
+            P[mb][nb][q] = sub_ref(P[mb][nb][q], kc, acc[mb][nb][q]);
+          }
+        }
         }
         if (p.variant == 1 && !last) drift_swap(wdrift(r));  // BAB: drift after kick r
       }
@@ -898,6 +934,13 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
       code = 1;
       fail_step = step_off + step;
       break;
+    }
+    if (fsal && step + 1 < L && !(xi > p.threshold)) {  // the next step's first kick, shared W
+      const double kf = wkick(0);
+      FOR_BLK {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) P[mb][nb][q] = sub_ref(P[mb][nb][q], kf, acc[mb][nb][q]);
+      }
     }
     if (xi > p.threshold) {
       // P <- P Q^-1, Q <- I (proposed.cpp:196-202)
@@ -941,7 +984,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
       }
       PROF_MARK(3);
       if (ok && p.residual_check)
-        ok = residual_ok<C>(Or, Oi, Sr, Si, [&](int mb, int nb, int q) { return P[mb][nb][q]; }, acc, own, n, *sc,
+        ok = residual_ok<C>(Or, Oi, Sr, Si, [&](int mb, int nb, int q) __attribute__((always_inline)) { return P[mb][nb][q]; }, acc, own, n, *sc,
                             warp, lane);
       if (!ok) {
         code = 2;
@@ -957,6 +1000,10 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
         ++rhst;
         if (!isfinite(xi)) ++npiv;
       }
+      if (fsal && step + 1 < L)
+        ukick(mbox, wkick(0));  // the next step's first kick, Q = I
+      else
+        qident = !RK4 && p.variant == 1;  // BAB: the next step opens with a kick on Q = I
       __syncthreads();
     }
     PROF_MARK(5);
@@ -975,19 +1022,12 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
     double* Or = Xr[2];  // saved Q: T and R are rebuilt bit-identically for the residual gate
     double* Oi = Xi[2];
     // T = G Q - i P, R = G Q + i P  (i*P = (-pi, pr)), own elements
-    auto tr = [&](int mb, int nb, const double (&q0)[4], double (&t)[4], double (&rr)[4]) {
+    auto tr = [&](int mb, int nb, const double (&q0)[4], double (&t)[4], double (&rr)[4]) __attribute__((always_inline)) {
       const int r = own.r(mb);
       const double2 g = r < n ? p.gdiag[pair * n + r] : make_double2(0.0, 0.0);
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const double qr = q0[e], qi = q0[2 + e];
-        const double gqr = g.x * qr - g.y * qi, gqi = g.x * qi + g.y * qr;
-        const double pr = P[mb][nb][e], pi = P[mb][nb][2 + e];
-        t[e] = gqr + pi;
-        t[2 + e] = gqi - pr;
-        rr[e] = gqr - pi;
-        rr[2 + e] = gqi + pr;
-      }
+      for (int e = 0; e < 2; ++e)
+        tau_rho_ref(g, q0[e], q0[2 + e], P[mb][nb][e], P[mb][nb][2 + e], t[e], t[2 + e], rr[e], rr[2 + e]);
     };
     __syncthreads();
     FOR_BLK {
@@ -1010,7 +1050,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
       __syncthreads();
       ok = residual_ok<C>(
           Ar, Ai, Er, Ei,
-          [&](int mb, int nb, int q) {
+          [&](int mb, int nb, int q) __attribute__((always_inline)) {
             double q0[4], t[4], rr[4];
             own.ld(Or, Oi, mb, nb, q0);
             tr(mb, nb, q0, t, rr);

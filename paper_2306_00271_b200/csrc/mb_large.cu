@@ -254,17 +254,15 @@ __global__ void __launch_bounds__(NTH, 2) big_stage_kernel(const __grid_constant
         pe[3] = b.y;
       }
       double K[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) K[q] = acc[mb][nb][q] + g2 * x[q];  // (U + G^2) X
       if (s.kind == 1) {  // splitting kick: P -= hb (U+G^2) Q ; optional drift Qn = Q + ha P
         double pv[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) pv[q] = pe[q] - s.c0 * K[q];
+        for (int q = 0; q < 4; ++q) pv[q] = kick_ref(pe[q], s.c0, acc[mb][nb][q], g2, x[q]);
         st(s.mp, o, pv);
         if (s.c1 != 0.0) {
           double qn[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) qn[q] = x[q] + s.c1 * pv[q];
+          for (int q = 0; q < 4; ++q) qn[q] = drift_ref(x[q], s.c1, pv[q]);
           st(s.mqn, o, qn);
         }
       } else {
@@ -272,7 +270,7 @@ __global__ void __launch_bounds__(NTH, 2) big_stage_kernel(const __grid_constant
         // resident kernel: K_s = -(U+G^2) X_s
         const double h = s.c0;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) K[q] = -K[q];
+        for (int q = 0; q < 4; ++q) K[q] = -(acc[mb][nb][q] + g2 * x[q]);  // -(U + G^2) X
         double pv[4] = {pe[0], pe[1], pe[2], pe[3]}, sq[4], w[4];
         if (s.kind == 3) {  // X = Q: SQ = K1, X3 = X2 + h^2/4 K1, W = Q + hP, P += h/6 K1
           double x2[4];
@@ -367,8 +365,8 @@ __global__ void big_elem_kernel(const __grid_constant__ BigParams p, const __gri
       const double* Q = mat(p, pair, s.mq);
       const double* P = mat(p, pair, s.mp);
       double* Qn = mat(p, pair, s.mqn);
-      Qn[o] = Q[o] + s.c1 * P[o];
-      Qn[NN + o] = Q[NN + o] + s.c1 * P[NN + o];
+      Qn[o] = drift_ref(Q[o], s.c1, P[o]);
+      Qn[NN + o] = drift_ref(Q[NN + o], s.c1, P[NN + o]);
     }
   }
 }
@@ -558,11 +556,7 @@ __global__ void __launch_bounds__(NTH, NPM == 128 ? 2 : 1) big_gj_kernel(const _
       const int r = (int)(o / np);
       const double2 gr = r < n ? G[r] : make_double2(0.0, 0.0);
       const double qr = Qm[o], qi = Qm[NN + o], pr = Pm[o], pi = Pm[NN + o];
-      const double gqr = gr.x * qr - gr.y * qi, gqi = gr.x * qi + gr.y * qr;
-      Sa[o] = gqr + pi;  // T = G Q - i P
-      Sa[NN + o] = gqi - pr;
-      Sb[o] = gqr - pi;  // R = G Q + i P
-      Sb[NN + o] = gqi + pr;
+      tau_rho_ref(gr, qr, qi, pr, pi, Sa[o], Sa[NN + o], Sb[o], Sb[NN + o]);  // T = G Q - i P, R = G Q + i P
     }
   }
   for (int c = tid; c < NPM; c += NTH) g.used[c] = c >= n;
