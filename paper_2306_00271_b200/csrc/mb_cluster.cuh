@@ -333,6 +333,71 @@ __device__ __forceinline__ void slab_gemm2(double (&acc)[C::MB][C::NB][4], const
     slab_gemm_ml<C, 1>(acc, box, soff, raddr, Xr, Xi, lane, kmax);
 }
 
+// Balanced product for a partial last round of row blocks. With LB = ceil(n/8)
+// live blocks, every warp owns MF = LB / 8 full blocks and warps 0..r-1 one
+// more (r = LB % 8; block 8 MF + e belongs to warp e), so the SMSPs hosting
+// warps < r carry up to 16% more DMMA work per kick (cfg3: 25 blocks, SMSP 0
+// 14 units vs 12). Here the U = r NB (block, column-block) units of that
+// round are shared by all 8 warps: warp w computes unit w / S over the k part
+// w % S (S = 8 / U), writes its 8x8 partial to shared memory, and after one
+// CTA barrier the owner warp sums the S parts in fixed order.
+template <class C>
+__device__ __forceinline__ void slab_gemm_split(double (&acc)[C::MB][C::NB][4], const double2* __restrict__ box,
+                                               const int* __restrict__ soff, const int (&raddr)[C::MB],
+                                               const double* __restrict__ Xr, const double* __restrict__ Xi, int mf,
+                                               int r, int S, int rau, double* __restrict__ part, int warp, int lane,
+                                               int kmax) {
+  constexpr int NB = C::NB;
+  slab_gemm2<C>(acc, box, soff, raddr, Xr, Xi, mf, lane, kmax);
+  const int kl = lane & 3, cl = lane >> 2;
+  const int u = warp / S, sp = warp % S, nb = u % NB;
+  const int ks = ((kmax >> 2) + S - 1) / S * 4;
+  const int kb = sp * ks, ke = min(kmax, kb + ks);
+  double t[2][3][2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int i = 0; i < 3; ++i) t[h][i][0] = t[h][i][1] = 0.0;
+  // two accumulator chains over alternate k-steps (hides the DMMA latency);
+  // k-steps past ke read in-bounds rows with a zero A operand
+#pragma unroll 1
+  for (int k0 = kb; k0 < ke; k0 += 8) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int k = min(k0 + 4 * h, kmax - 4) + kl;
+      const bool in = k0 + 4 * h < ke;
+      const double2 a = (in && rau >= 0) ? box[rau - soff[k]] : make_double2(0.0, 0.0);
+      const int o = ss<C::SW>(k, nb * 8 + cl);
+      const double xr = Xr[o], xi = Xi[o];
+      dmma(t[h][0][0], t[h][0][1], a.x, xr);
+      dmma(t[h][1][0], t[h][1][1], a.y, xi);
+      dmma(t[h][2][0], t[h][2][1], a.x + a.y, xr + xi);
+    }
+  }
+  double* const mine = part + (size_t)warp * 128 + lane * 4;  // unit u, part sp = slot warp
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const double t1 = t[0][0][e] + t[1][0][e], t2 = t[0][1][e] + t[1][1][e], t3 = t[0][2][e] + t[1][2][e];
+    mine[e] = t1 - t2;
+    mine[2 + e] = (t3 - t1) - t2;
+  }
+  __syncthreads();
+  if (warp < r) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int slot0 = (warp * NB + b) * S;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        double v = part[(size_t)slot0 * 128 + lane * 4 + q];
+        for (int s2 = 1; s2 < S; ++s2) v += part[(size_t)(slot0 + s2) * 128 + lane * 4 + q];
+#pragma unroll
+        for (int m = 0; m < C::MB; ++m)
+          if (m == mf) acc[m][b][q] = v;
+      }
+    }
+  }
+}
+
 // residual tile configuration (SW rows x NP/8 columns per warp)
 template <int NP_, int SW_>
 struct RCfg {
@@ -517,6 +582,14 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
   int ml = 0;  // live row blocks of this warp (blocks m < ml)
 #pragma unroll
   for (int m = 0; m < MB; ++m) ml += live(m) ? 1 : 0;
+  // balanced split of a partial last round of row blocks (slab_gemm_split)
+  const int lblk = (n + 7) / 8, smf = lblk / CNW, sr = lblk % CNW;
+  const int sS = (sr > 0 && smf > 0 && (CNW % (sr * NB)) == 0) ? CNW / (sr * NB) : 0;
+  int srau = -1;  // raddr of the lane's row in the warp's shared unit
+  if (sS) {
+    const int row = 8 * (CNW * smf + (warp / sS) / NB) + (lane >> 2);
+    srau = row < n ? p.box_center + p.rowoff[row] : -1;
+  }
   auto ld = [&](const double* Xr, const double* Xi, int m, int nb, double (&v)[4]) MB_INL {
     const int o = ss<SW>(orow(m), ocol(nb));
     const double2 a = *reinterpret_cast<const double2*>(Xr + o);
@@ -1167,7 +1240,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
         st(Yr, Yi, m, nb, v);
       }
       double2* box = begin_occ(step, 1);
-      slab_gemm2<C>(acc, box, soff, raddr, Qr, Qi, ml, lane, kmax);
+      if (sS) slab_gemm_split<C>(acc, box, soff, raddr, Qr, Qi, smf, sr, sS, srau, wchr, warp, lane, kmax); else slab_gemm2<C>(acc, box, soff, raddr, Qr, Qi, ml, lane, kmax);
       CPROF(1);
       end_occ(step, 1);
       FOR_OWN {
@@ -1197,7 +1270,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
         st(Qr, Qi, m, nb, q0);
       }
       box = begin_occ(step, 2);
-      slab_gemm2<C>(acc, box, soff, raddr, Yr, Yi, ml, lane, kmax);
+      if (sS) slab_gemm_split<C>(acc, box, soff, raddr, Yr, Yi, smf, sr, sS, srau, wchr, warp, lane, kmax); else slab_gemm2<C>(acc, box, soff, raddr, Yr, Yi, ml, lane, kmax);
       CPROF(1);
       end_occ(step, 2);
       FOR_OWN {
@@ -1228,7 +1301,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
         st(Qr, Qi, m, nb, qb);
       }
       box = begin_occ(step, 3);
-      slab_gemm2<C>(acc, box, soff, raddr, Zr, Zi, ml, lane, kmax);
+      if (sS) slab_gemm_split<C>(acc, box, soff, raddr, Zr, Zi, smf, sr, sS, srau, wchr, warp, lane, kmax); else slab_gemm2<C>(acc, box, soff, raddr, Zr, Zi, ml, lane, kmax);
       CPROF(1);
       end_occ(step, 3);
       FOR_OWN {
@@ -1246,7 +1319,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
         st(Qr, Qi, m, nb, qb);
       }
       box = begin_occ(step + 1, 0);
-      slab_gemm2<C>(acc, box, soff, raddr, Yr, Yi, ml, lane, kmax);
+      if (sS) slab_gemm_split<C>(acc, box, soff, raddr, Yr, Yi, smf, sr, sS, srau, wchr, warp, lane, kmax); else slab_gemm2<C>(acc, box, soff, raddr, Yr, Yi, ml, lane, kmax);
       CPROF(1);
       end_occ(step + 1, 0);
       FOR_OWN {
@@ -1277,7 +1350,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
           end_occ(nstep, nr);
           qident = false;
         } else {
-        slab_gemm2<C>(acc, box, soff, raddr, Ar, Ai, ml, lane, kmax);
+        if (sS) slab_gemm_split<C>(acc, box, soff, raddr, Ar, Ai, smf, sr, sS, srau, wchr, warp, lane, kmax); else slab_gemm2<C>(acc, box, soff, raddr, Ar, Ai, ml, lane, kmax);
       CPROF(1);
         end_occ(nstep, nr);
         if (last) mbox = box;  // FSAL: node of the next step's first kick
