@@ -437,6 +437,8 @@ struct mb_plan {
   mbx::PotentialParams pot{};
   mbx::PropagateParams prop{};
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  cudaStream_t side = nullptr;  // batched path: second half-batch stream
+  cudaEvent_t fork = nullptr, join = nullptr;
   float ms_total = 0, ms_pot = 0, ms_prop = 0;
   int launches = 0;
   long h2d_bytes = 0;
@@ -482,6 +484,9 @@ void free_plan(mb_plan* pl) {
   }
   for (cudaEvent_t& e : pl->ev)
     if (e) cudaEventDestroy(e);
+  if (pl->fork) cudaEventDestroy(pl->fork);
+  if (pl->join) cudaEventDestroy(pl->join);
+  if (pl->side) cudaStreamDestroy(pl->side);
   delete pl;
 }
 
@@ -620,16 +625,18 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
 
   // auto: the cluster kernel keeps the state on chip but spans CS SMs per pair
   // and serialises its Gauss-Jordan over the cluster; the batched path
-  // amortises its per-pair solves over many pairs. Measured crossover (B200,
-  // round 1): cluster wins for the 61-pair N=199 case, the batched path for
-  // 4096 pairs at N=127/255.
+  // amortises its per-pair solves over many pairs. Measured (B200, round 2,
+  // tools/cmp_paths.py, 4096 pairs): splitting steppers are faster on the
+  // cluster kernel at any batch size (N=127 sp6 25.8 vs 24.8 TF/s, N=255 sp6
+  // 30.2 vs 28.0); rk4 keeps the batched path from 512 pairs (N=127: 20.8 vs
+  // 18.5), where its four stage products per step amortise the per-pair solves.
   bool cluster = false;
   if (conv) big = false;
   // bulk seeding (per-pair period loop until R settles) exists only in the
   // on-chip kernels, so it takes the cluster kernel at any batch size
   const bool want_cluster = opts->path == 3 || opts->path == 4;
-  if (big && (want_cluster || (opts->path == 0 && (npairs < 512 || bulk)))) {
-    const int rk4 = stepper->algorithm == MB_STEP_RK4;
+  const int rk4 = stepper->algorithm == MB_STEP_RK4;
+  if (big && (want_cluster || (opts->path == 0 && (npairs < 512 || bulk || !rk4)))) {
     const size_t need = mbx::cluster_smem_bytes(n, rk4, box_size, ndiff);
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
@@ -886,11 +893,73 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
 
 // Large-N orchestration: one launch per kick / RK stage over all pairs, then
 // the per-pair check and RHST kernels each step; the surface solve at the end.
+// The batched path as two half-batches on two streams. Per step a
+// half-batch runs its stage products, the row-block check and the per-pair
+// Gauss-Jordan; the solve launch keeps few CTAs busy (only the pairs that
+// RHST at this step), so the other half's stage products fill the SMs
+// meanwhile. Launches are issued step by step, alternating halves, so neither
+// stream's queue runs ahead of the other. Pairs are independent: the halves
+// give bitwise the rows of one batch.
+mbx::BigParams big_part(const mbx::BigParams& b, long lo, long hi) {
+  mbx::BigParams h = b;
+  const long chk_per = (long)((b.np + 15) / 16) * 4;
+  h.npairs = hi - lo;
+  h.pair_struct = b.pair_struct + lo;
+  h.gamma2 = b.gamma2 + lo * b.n;
+  h.gdiag = b.gdiag + lo * b.n;
+  h.ginv = b.ginv + lo * b.n;
+  h.sin_theta0 = b.sin_theta0 + lo;
+  h.state = b.state + lo * b.pair_stride;
+  h.status = b.status + lo;
+  h.xi = b.xi + lo;
+  h.chk = b.chk + lo * chk_per;
+  h.chk_count = b.chk_count + lo;
+  h.eta = b.eta + lo * b.n;
+  h.rho = b.rho + lo * b.n;
+  return h;
+}
+
 void execute_big(mb_plan* pl, cudaStream_t st) {
-  const mbx::BigParams& b = pl->bp;
   const mbx::PropagateParams& p = pl->prop;
   int* nl = &pl->launches;
-  auto launch = [&](const mbx::BigStage& s) { cuda_check(mbx::big_launch_stage(b, s, st, nl), "big stage launch"); };
+  // two halves from 1024 pairs (each half still fills the GPU with tiles)
+  const bool two = pl->bp.npairs >= 1024;
+  std::vector<mbx::BigParams> part;
+  std::vector<cudaStream_t> sts;
+  if (two) {
+    if (!pl->side) {
+      cuda_check(cudaStreamCreateWithFlags(&pl->side, cudaStreamNonBlocking), "cudaStreamCreate");
+      cuda_check(cudaEventCreateWithFlags(&pl->fork, cudaEventDisableTiming), "cudaEventCreate");
+      cuda_check(cudaEventCreateWithFlags(&pl->join, cudaEventDisableTiming), "cudaEventCreate");
+    }
+    const long half = pl->bp.npairs / 2;
+    part = {big_part(pl->bp, 0, half), big_part(pl->bp, half, pl->bp.npairs)};
+    sts = {st, pl->side};
+    cuda_check(cudaEventRecord(pl->fork, st), "event");
+    cuda_check(cudaStreamWaitEvent(pl->side, pl->fork, 0), "stream wait");
+  } else {
+    part = {pl->bp};
+    sts = {st};
+  }
+  const int H = (int)part.size();
+  auto launch = [&](const mbx::BigStage& s) {
+    for (int h = 0; h < H; ++h) cuda_check(mbx::big_launch_stage(part[h], s, sts[h], nl), "big stage launch");
+  };
+  auto check_and_solve = [&](int step, int mq, int mp, int msa, int msb, int mx2, double hh) {
+    for (int h = 0; h < H; ++h) {
+      cuda_check(mbx::big_launch_check(part[h], step, mq, mp, sts[h], nl), "big check launch");
+      cuda_check(mbx::big_launch_gj(part[h], 0, step, mq, mp, msa, msb, mx2, hh, sts[h], nl), "big RHST launch");
+    }
+  };
+  auto surface = [&](int mq, int mp, int msa, int msb) {
+    for (int h = 0; h < H; ++h)
+      cuda_check(mbx::big_launch_gj(part[h], 1, p.nsteps, mq, mp, msa, msb, -1, 0.0, sts[h], nl),
+                 "big surface-solve launch");
+    if (two) {
+      cuda_check(cudaEventRecord(pl->join, pl->side), "event");
+      cuda_check(cudaStreamWaitEvent(st, pl->join, 0), "stream wait");
+    }
+  };
   auto slot = [&](int step, int r) { return (long)step * pl->stride + p.occ_node[r]; };
   mbx::BigStage s{};
   const int L = p.nsteps;
@@ -904,10 +973,9 @@ void execute_big(mb_plan* pl, cudaStream_t st) {
         s = mbx::BigStage{3 + k, ops[k], slot(step, k), step, p.h, 0.0, 0.0, Q, -1, P, X2, X3, W, V, SQ};
         launch(s);
       }
-      cuda_check(mbx::big_launch_check(b, step, Q, P, st, nl), "big check launch");
-      cuda_check(mbx::big_launch_gj(b, 0, step, Q, P, X3, V, X2, p.h, st, nl), "big RHST launch");
+      check_and_solve(step, Q, P, X3, V, X2, p.h);
     }
-    cuda_check(mbx::big_launch_gj(b, 1, L, Q, P, X3, V, -1, 0.0, st, nl), "big surface-solve launch");
+    surface(Q, P, X3, V);
     return;
   }
   const int P = 2, SCR = 3;
@@ -919,32 +987,25 @@ void execute_big(mb_plan* pl, cudaStream_t st) {
   // reference's two roundings around the end-of-step check (see the on-chip
   // kernels), and here the shared product would be an extra N x N plane per
   // pair in HBM. Unmerged kicks give exactly the fsal = 0 results.
-  const bool fsal = false;
   auto drift = [&](double c) {
     mbx::BigStage d{2, 0, 0, 0, 0.0, c, 0.0, qc, qc ^ 1, P, -1, -1, -1, -1, -1};
     launch(d);
     qc ^= 1;
   };
   for (int step = 0; step < L; ++step) {
-    int r0 = 0;
-    if (fsal && step > 0) {
-      drift(p.occ_drift[0]);
-      r0 = 1;
-    }
-    for (int r = r0; r < nk; ++r) {
+    for (int r = 0; r < nk; ++r) {
       const bool last = r == nk - 1;
       if (p.variant == 0) drift(p.occ_drift[r]);
-      const double kc = (fsal && last && step + 1 < L) ? p.fsal_kick : p.occ_kick[r];
+      const double kc = p.occ_kick[r];
       const double dc = (p.variant == 1 && !last) ? p.occ_drift[r] : 0.0;
       mbx::BigStage k{1, qc, slot(step, r), step, kc, dc, 0.0, qc, qc ^ 1, P, -1, -1, -1, -1, -1};
       launch(k);
       if (dc != 0.0) qc ^= 1;
     }
     if (p.variant == 0) drift(p.final_drift);
-    cuda_check(mbx::big_launch_check(b, step, qc, P, st, nl), "big check launch");
-    cuda_check(mbx::big_launch_gj(b, 0, step, qc, P, qc ^ 1, SCR, -1, 0.0, st, nl), "big RHST launch");
+    check_and_solve(step, qc, P, qc ^ 1, SCR, -1, 0.0);
   }
-  cuda_check(mbx::big_launch_gj(b, 1, L, qc, P, qc ^ 1, SCR, -1, 0.0, st, nl), "big surface-solve launch");
+  surface(qc, P, qc ^ 1, SCR);
 }
 
 void execute_plan(mb_plan* pl, cudaStream_t st) {

@@ -1203,11 +1203,13 @@ static cudaError_t launch_cfg(const PropagateParams& p, cudaStream_t st) {
 // tile (C64) with the K-sum folded into the Q plane (16 warps spill)
 // tile variants (WM, WN, CTAs/SM) selectable at build time for tuning sweeps
 // (round-1 sweep on B200, tools/sweep.py cfg2 + cfg4 N=15/31: 4 warps x 3
-// CTAs/SM at NP=32 beat 8 warps x 2 by 12% for rk4 and 3% for sp6)
+// CTAs/SM at NP=32 beat 8 warps x 2 by 12% for rk4 and 3% for sp6; round 2:
+// splitting at NP=32 takes 2 CTAs/SM, since its 3-CTA register cap (170)
+// spilled the reference-rounding epilogue: N=31 sp6 14.9K -> 17.9K points/s)
 #ifndef MB_C32_WM
 #define MB_C32_WM 2
 #define MB_C32_WN 2
-#define MB_C32_MINB 3
+#define MB_C32_MINB 2
 #endif
 #ifndef MB_C32R_WM
 #define MB_C32R_WM 2

@@ -1,6 +1,8 @@
 """Full-size sweep of the five BASELINE configs: one plan execute per case,
 device time from CUDA events (mb_plan_timing), algorithmic TFLOP/s
-(L * s_eff * 8 N^3 per point). JSON line per case."""
+(L * s_eff * 8 N^3 per point), fraction of the measured
+DMMA peak, and the nvidia-smi clock record of the timed executes (bench.py's
+Clocks: median SM clock, max clock, throttle reasons). JSON line per case."""
 import argparse
 import json
 import os
@@ -13,6 +15,7 @@ import numpy as np  # noqa: E402
 
 import paper_2306_00271_b200 as mb  # noqa: E402
 from paper_2306_00271_b200 import configs  # noqa: E402
+from bench import Clocks, fp64_peaks  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--cases", default="0,1,2,3,4")
@@ -40,10 +43,14 @@ for w in cases:
     plan = mb.Plan(rods, configs.product_fields(w), w.gamma, pairs, opts, ctx)
     t_plan = time.perf_counter() - t0
     best = None
+    plan.execute()  # warm-up (first-touch of the table, clocks up)
+    ck = Clocks(0)
+    ck.start()
     for _ in range(a.reps):
         plan.execute()
         t = plan.timing()
         best = t if best is None or t["ms_total"] < best["ms_total"] else best
+    clocks = ck.stop()
     eta, rho, st = plan.results(raise_on_error=False)
     info = plan.info()
     plan.close()
@@ -53,5 +60,9 @@ for w in cases:
                       "ms_propagate": best["ms_propagate"], "launches": best["launches"],
                       "points_per_s": len(pairs) / (best["ms_total"] * 1e-3),
                       "tflops_propagate": flops / (best["ms_propagate"] * 1e-3) / 1e12,
+                      "frac_dmma_peak": flops / (best["ms_propagate"] * 1e-3) / 1e12 / fp64_peaks()[0],
+                      "path": ("resident" if info["npad"] <= 64 else "on-chip (cluster / cooperative groups)"
+                               if w.method != "rk4" or len(pairs) < 512 else "batched"),
+                      "clocks": clocks,
                       "rhst_per_point": float(st["rhst"].mean()), "rhst_pivoting_per_point": float(st["rhst_pivoting"].mean()), "failed": int((st["code"] != 0).sum()),
                       "npad": info["npad"], "plan_s": t_plan}), flush=True)
