@@ -68,7 +68,7 @@ namespace mbx {
 namespace {
 
 constexpr int CNT = 256, CNW = 8;
-constexpr int WCH = 32;  // columns per DSMEM chunk of the blocked solve
+constexpr int WCH = 32;  // sizes the partials area (8 warps x 128 doubles at SW = 16)
 
 // SW = slab columns per CTA = rows per CTA in the solve layout (16 at NP=256,
 // 32 at NP=128: the wider slab gives the warps C64's 16x32 tile)
@@ -110,8 +110,8 @@ __host__ __device__ inline Layout cluster_layout(int np, int SW, int nq, int box
   o += al16((size_t)(3 * SW + 1) * sizeof(double2));
   L.tloc = o;  // special columns, pivot slots, mask; F on special columns; 1/pivots, |pivot|^2
   o += al16((size_t)(8 * SW + 2 * SW * SW + 2 * SW) * sizeof(double2));
-  L.wch = o;  // W chunk: 16 panel rows x WCH columns, re/im
-  o += al16((size_t)2 * SW * WCH * sizeof(double));
+  L.wch = o;  // k-split partials of the product; x of the solve's rank-SW update
+  o += al16((size_t)2 * SW * (WCH > SW + 8 ? WCH : SW + 8) * sizeof(double));
   L.scr = o;
   o += al16(sizeof(Scratch));
   L.g2s = o;
@@ -460,8 +460,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
                                                          2 * NP + 8)
                              : reinterpret_cast<double2*>(smem + LY.tpub);  // panel table
   double2* const tloc = reinterpret_cast<double2*>(smem + LY.tloc);  // consumer tables
-  double* const wchr = reinterpret_cast<double*>(smem + LY.wch);     // [16][WCH]
-  double* const wchi = wchr + SW * WCH;
+  double* const wchr = reinterpret_cast<double*>(smem + LY.wch);     // product partials / solve x
   Scratch* const sc = reinterpret_cast<Scratch*>(smem + LY.scr);
   double* const g2s = reinterpret_cast<double*>(smem + LY.g2s);
   // published arrays, read by the other CTAs of the group: shared memory
@@ -919,53 +918,77 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
         }
       }
       CPROF(7);  // special columns
-      // (B) other columns: X[i][j] -= sum_k x_k F_k[j] (F_k[j] = A[k][j]),
-      // F chunks from the owner through DSMEM, next chunk prefetched into
-      // registers while the current one is applied
-      // SW x WCH chunk, FR double2 per thread and plane
-      constexpr int FR = SW * (WCH / 2) / CNT;
-      auto fetch = [&](int j0, double2 (&a)[FR], double2 (&c)[FR]) MB_INL {
+      // (B) other columns: X[i][j] -= sum_k x_k(i) F_k[j] (F_k[j] = A[k][j])
+      // on the FP64 tensor pipe: x (own rows x panel k) staged in shared
+      // memory is the A operand, the owner's panel rows F (L2) the B operand
+      // and the own X tile the accumulator; four real products per complex
+      // 8x8 block k-step, no 3M sums. Warp w takes column blocks w, w + 8, ...;
+      // every F fragment it needs is loaded up front. Stores are masked to the
+      // non-special columns < n of rows < n (the special columns are final).
+      constexpr int XLD = SW + 8;  // k-major x: A fragments in two wavefronts
+      constexpr int KS = SW / 4, RBK = SW / 8, CBW = NP / 64;
+      double* const xsr = wchr;
+      double* const xsi = wchr + SW * XLD;
+      if (cg == 0) {
 #pragma unroll
-        for (int f = 0; f < FR; ++f) {
-          const int w = tid + f * CNT, ldt = w / (WCH / 2), j = j0 + 2 * (w % (WCH / 2));
-          a[f] = make_double2(0.0, 0.0);
-          c[f] = a[f];
-          if (ldt < nk && j < NP) {
-            const long o = (long)ldt * NP + j;
-            a[f] = __ldcg(reinterpret_cast<const double2*>(war + o));
-            c[f] = __ldcg(reinterpret_cast<const double2*>(wai + o));
-          }
-          if (j >= n || ((smask[j >> 5] >> (j & 31)) & 1u)) a[f].x = c[f].x = 0.0;
-          if (j + 1 >= n || ((smask[(j + 1) >> 5] >> ((j + 1) & 31)) & 1u)) a[f].y = c[f].y = 0.0;
+        for (int lk = 0; lk < SW; ++lk) {
+          xsr[lk * XLD + lr] = act ? xk[lk].x : 0.0;
+          xsi[lk * XLD + lr] = act ? xk[lk].y : 0.0;
         }
-      };
-      double2 na[FR], nc[FR];
-      fetch(0, na, nc);
-      for (int j0 = 0; j0 < n; j0 += WCH) {
-        __syncthreads();  // previous chunk consumed (and the special write-back done)
+      }
+      const int kl = lane & 3, cl = lane >> 2, ncb = (n + 7) >> 3;
+      double fr[CBW][KS], fi[CBW][KS];
 #pragma unroll
-        for (int f = 0; f < FR; ++f) {
-          const int w = tid + f * CNT, ldt = w / (WCH / 2), ldj = 2 * (w % (WCH / 2));
-          *reinterpret_cast<double2*>(wchr + ldt * WCH + ldj) = na[f];
-          *reinterpret_cast<double2*>(wchi + ldt * WCH + ldj) = nc[f];
+      for (int c = 0; c < CBW; ++c) {
+        const int j = 8 * (warp + 8 * c) + cl;
+#pragma unroll
+        for (int s = 0; s < KS; ++s) {
+          const int k = 4 * s + kl;
+          const bool ok = k < nk && j < n;
+          const long o = (long)k * NP + j;
+          fr[c][s] = ok ? __ldcg(war + o) : 0.0;
+          fi[c][s] = ok ? __ldcg(wai + o) : 0.0;
         }
-        __syncthreads();
-        if (j0 + WCH < n) fetch(j0 + WCH, na, nc);
-        if (act) {
+      }
+      __syncthreads();  // x staged (and the special columns written back)
 #pragma unroll
-          for (int u = 0; u < WCH / TPR; ++u) {
-            const int jj = cg + TPR * u, j = j0 + jj;
-            if (j >= n) continue;
-            const int o = sw<NP>(lr, j);
-            double xr = Xr[o], xi = Xi[o];
+      for (int c = 0; c < CBW; ++c) {
+        const int cb = warp + 8 * c;
+        if (cb < ncb) {
+          const int j = 8 * cb + 2 * kl;
+          const bool s0 = j < n && !((smask[j >> 5] >> (j & 31)) & 1u);
+          const bool s1 = j + 1 < n && !((smask[(j + 1) >> 5] >> ((j + 1) & 31)) & 1u);
 #pragma unroll
-            for (int t = 0; t < SW; ++t) {
-              const double wr = wchr[t * WCH + jj], wi = wchi[t * WCH + jj];
-              xr -= xk[t].x * wr - xk[t].y * wi;
-              xi -= xk[t].x * wi + xk[t].y * wr;
+          for (int rb = 0; rb < RBK; ++rb) {
+            const int r = 8 * rb + cl;
+            const int o = sw<NP>(r, j);
+            const double2 cr = *reinterpret_cast<const double2*>(Xr + o);
+            const double2 ci = *reinterpret_cast<const double2*>(Xi + o);
+            double c0 = cr.x, c1 = cr.y, d0 = ci.x, d1 = ci.y;
+#pragma unroll
+            for (int s = 0; s < KS; ++s) {
+              const int ai = (4 * s + kl) * XLD + r;
+              const double ar = xsr[ai], aim = xsi[ai];
+              dmma(c0, c1, dneg(ar), fr[c][s]);
+              dmma(c0, c1, aim, fi[c][s]);
+              dmma(d0, d1, dneg(ar), fi[c][s]);
+              dmma(d0, d1, dneg(aim), fr[c][s]);
             }
-            Xr[o] = xr;
-            Xi[o] = xi;
+            if (col0 + r < n) {
+              if (s0 && s1) {
+                *reinterpret_cast<double2*>(Xr + o) = make_double2(c0, c1);
+                *reinterpret_cast<double2*>(Xi + o) = make_double2(d0, d1);
+              } else {
+                if (s0) {
+                  Xr[o] = c0;
+                  Xi[o] = d0;
+                }
+                if (s1) {
+                  Xr[o + 1] = c1;
+                  Xi[o + 1] = d1;
+                }
+              }
+            }
           }
         }
       }
