@@ -90,7 +90,8 @@ typedef struct {
   int has_bulk_period; /* bulk seed R_init per pair (compute_bulk_reflection_proposed,
                           proposed.cpp:311-342): resident kernel (N <= 64) and cluster
                           kernel (64 < N <= 256; rk4 only up to N = 128); other
-                          cases return MB_ERR_CONFIG */
+                          cases return MB_ERR_CONFIG. A caller-supplied R_init
+                          (mb_plan_create_seeded) replaces it. */
   double bulk_period;
   /* MB_FIELD_GAUSSIAN_LAYERS: layers[nlayers][5] = z_center, amplitude,
    * sigma_xy, sigma_z, absorption */
@@ -206,6 +207,21 @@ int mb_device_ok(int device);
 int mb_plan_create(mb_context* ctx, const mb_rods* rods, const mb_field* fields, int nfields,
                    double gamma, const mb_pair* pairs, long npairs, const mb_stepper* stepper,
                    const mb_options* opts, mb_plan** out);
+/* The same with a caller-supplied R_init: solve_proposed(u, gamma, plan, spec,
+ * opts, R_init, ...) (proposed.hpp:98-102; initial_state, proposed.cpp:123-128:
+ * T = I, R = R_init at z_bottom). r_init holds r_init_count matrices of
+ * n x n complex128, row-major, interleaved (re, im): count 1 = one R_init
+ * shared by every pair, count npairs = one per pair (pair order). It is used
+ * as given, so a field's bulk period is NOT solved for (the reference's
+ * solve_row passes its bulk R the same way, sweep.cpp:96-101). Null r_init
+ * with count 0 is mb_plan_create. Every design takes it (resident, cluster /
+ * cooperative, batched, any device count); MB_STEP_CONVENTIONAL does not
+ * (MB_ERR_CONFIG). A wrong count is MB_ERR_ARG ("R_init has wrong
+ * dimensions", proposed.cpp:126). */
+int mb_plan_create_seeded(mb_context* ctx, const mb_rods* rods, const mb_field* fields, int nfields,
+                          double gamma, const mb_pair* pairs, long npairs, const mb_stepper* stepper,
+                          const mb_options* opts, const double* r_init, long r_init_count,
+                          mb_plan** out);
 /* K1 (slice-potential coefficients) + K2 (propagation, RHST, extraction,
  * intensity). Inputs already device-resident; stream 0 = context stream. */
 int mb_plan_execute(mb_plan* plan, void* cuda_stream);

@@ -367,6 +367,48 @@ inline RockingCurve rocking_curve(const PotentialField& field, const RodSet& rod
   return c;
 }
 
+// proposed.hpp:94-102 (SolveStats, solve_proposed): one beam direction,
+// the state seeded with a caller-supplied R_init (n x n row-major; empty =
+// zero, initial_state proposed.cpp:123-128) at z_bottom; returns rho0, the
+// first column of R at the surface. Errors as the reference: "R_init has
+// wrong dimensions" (SolverError, proposed.cpp:126), BreakdownError with the
+// step for a nonfinite state, a failed RHST or a failed extraction.
+struct SolveStats {
+  long rhst_transforms = 0;
+};
+
+inline std::vector<Complex> solve_proposed(const PotentialField& field, const RodSet& rods, double gamma,
+                                           double theta0_deg, double theta1_deg, const SweepOptions& opts,
+                                           const std::vector<Complex>& R_init = {}, SolveStats* stats = nullptr) {
+  const std::size_t n = (std::size_t)rods.size();
+  if (!R_init.empty() && R_init.size() != n * n) throw SolverError("R_init has wrong dimensions");
+  mb_stepper st{};
+  check(mb_stepper_by_name(opts.method.c_str(), &st));
+  if (st.algorithm == MB_STEP_CONVENTIONAL) throw ConfigError("solve_proposed: rk4, sp4 or sp6");
+  const mb_options o{opts.dz, opts.slices, opts.rhst_threshold, opts.residual_check ? 1 : 0, opts.fsal ? 1 : 0, 0};
+  const mb_field f = field.view();
+  const mb_rods r = rods.view();
+  const mb_pair pair{0, theta0_deg, theta1_deg};
+  mb_context* ctx = context(opts.device);
+  struct Guard {
+    mb_plan* p = nullptr;
+    ~Guard() {
+      if (p) mb_plan_destroy(p);
+    }
+  } g;
+  check(mb_plan_create_seeded(ctx, &r, &f, 1, gamma, &pair, 1, &st, &o,
+                              R_init.empty() ? nullptr : reinterpret_cast<const double*>(R_init.data()),
+                              R_init.empty() ? 0 : 1, &g.p));
+  check(mb_plan_execute(g.p, nullptr));
+  std::vector<double> eta(n);
+  std::vector<Complex> rho(n);
+  mb_point_status ps{};
+  const int rc = mb_plan_results(g.p, eta.data(), reinterpret_cast<double*>(rho.data()), &ps);
+  check(rc, (std::size_t)ps.step);
+  if (stats) stats->rhst_transforms = ps.rhst_count;
+  return rho;
+}
+
 // curve.cpp:22-41
 inline double curve_error(const RockingCurve& cand, const RockingCurve& ref) {
   if (cand.rows() != ref.rows()) throw CompareError("curve_error: row count mismatch");

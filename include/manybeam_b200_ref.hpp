@@ -15,7 +15,9 @@
 #pragma once
 
 #include <manybeam/curve.hpp>
+#include <manybeam/geometry.hpp>
 #include <manybeam/potential.hpp>
+#include <manybeam/proposed.hpp>
 #include <manybeam/rods.hpp>
 #include <manybeam/sweep.hpp>
 #include <manybeam/types.hpp>
@@ -83,19 +85,11 @@ inline manybeam::RockingCurve from_device(const RockingCurve& c, const manybeam:
   return out;
 }
 
-// sweep.hpp:37-38 on the device; the reference's exception types
-inline manybeam::RockingCurve rocking_curve(const manybeam::PotentialField& field, const manybeam::RodSet& rods,
-                                            double gamma, const manybeam::AngleGrid& grid,
-                                            const manybeam::SweepOptions& opts, int device = 0) {
+// device exception -> the reference's exception types (types.hpp:20-62)
+template <class F>
+auto with_reference_errors(F&& body) -> decltype(body()) {
   try {
-    SweepOptions o;
-    o.method = opts.method;
-    o.dz = opts.dz;
-    o.rhst_threshold = opts.rhst_threshold;
-    o.device = device;
-    return from_device(rocking_curve(to_device(field), to_device(rods), gamma,
-                                     AngleGrid::validated(grid.theta0, grid.theta1), o),
-                       rods);
+    return body();
   } catch (const BreakdownError& e) {
     throw manybeam::BreakdownError(e.what(), e.step);
   } catch (const ConvergenceError& e) {
@@ -113,6 +107,86 @@ inline manybeam::RockingCurve rocking_curve(const manybeam::PotentialField& fiel
   } catch (const IoError& e) {
     throw manybeam::IoError(e.what());
   }
+}
+
+// sweep.hpp:37-38 on the device; the reference's exception types
+inline manybeam::RockingCurve rocking_curve(const manybeam::PotentialField& field, const manybeam::RodSet& rods,
+                                            double gamma, const manybeam::AngleGrid& grid,
+                                            const manybeam::SweepOptions& opts, int device = 0) {
+  return with_reference_errors([&] {
+    SweepOptions o;
+    o.method = opts.method;
+    o.dz = opts.dz;
+    o.rhst_threshold = opts.rhst_threshold;
+    o.device = device;
+    return from_device(rocking_curve(to_device(field), to_device(rods), gamma,
+                                     AngleGrid::validated(grid.theta0, grid.theta1), o),
+                       rods);
+  });
+}
+
+// solve_proposed (proposed.hpp:98-102, proposed.cpp:293-309) on the device:
+// rho0 for one beam from the state seeded with R_init (empty = zero) at
+// plan.z_bottom, any StepperSpec (rk4, sp4, sp6 or a custom splitting). The
+// reference call takes the BoundPotential and the GammaMatrix; the device
+// builds both itself, so the adapter takes what they are built from (the
+// field with its rods, and the beam). The UTable argument has no counterpart:
+// the device's coefficient table always exists.
+inline manybeam::ComplexVector solve_proposed(const manybeam::PotentialField& field, const manybeam::RodSet& rods,
+                                              const manybeam::BeamGeometry& beam, const manybeam::SlicingPlan& plan,
+                                              const manybeam::StepperSpec& spec,
+                                              const manybeam::ProposedOptions& opts = {},
+                                              const manybeam::ComplexMatrix& R_init = manybeam::ComplexMatrix(),
+                                              manybeam::SolveStats* stats = nullptr, int device = 0) {
+  return with_reference_errors([&] {
+    spec.validate();
+    const int n = rods.size();
+    if (R_init.size() != 0 && (R_init.rows() != n || R_init.cols() != n))
+      throw SolverError("R_init has wrong dimensions");  // proposed.cpp:126
+    if (plan.z_bottom != field.z_bottom()) throw SolverError("slicing plan and field disagree on z_bottom");
+    std::vector<double> seed;  // row-major interleaved (the C-ABI layout)
+    if (R_init.size() != 0)
+      for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+          seed.push_back(R_init(i, j).real());
+          seed.push_back(R_init(i, j).imag());
+        }
+    mb_stepper st{};
+    if (spec.algorithm == manybeam::StepAlgorithm::RK4) {
+      st.algorithm = MB_STEP_RK4;
+      st.variant = MB_SPLIT_BAB;
+    } else {
+      st.algorithm = MB_STEP_SPLITTING;
+      st.variant = spec.variant == manybeam::SplitVariant::ABA ? MB_SPLIT_ABA : MB_SPLIT_BAB;
+      st.ndrift = (int)spec.drift.size();
+      st.drift = spec.drift.data();
+      st.nkick = (int)spec.kick.size();
+      st.kick = spec.kick.data();
+    }
+    const mb_options o{plan.h, plan.count, opts.rhst_threshold, 1, 0, 0};
+    const PotentialField df = to_device(field);
+    const RodSet dr = to_device(rods);
+    const mb_field f = df.view();
+    const mb_rods r = dr.view();
+    const mb_pair pair{0, beam.theta0_deg, beam.theta1_deg};
+    struct Guard {
+      mb_plan* p = nullptr;
+      ~Guard() {
+        if (p) mb_plan_destroy(p);
+      }
+    } g;
+    check(mb_plan_create_seeded(context(device), &r, &f, 1, beam.gamma, &pair, 1, &st, &o,
+                                seed.empty() ? nullptr : seed.data(), seed.empty() ? 0 : 1, &g.p));
+    check(mb_plan_execute(g.p, nullptr));
+    std::vector<double> eta((std::size_t)n);
+    std::vector<Complex> rho((std::size_t)n);
+    mb_point_status ps{};
+    check(mb_plan_results(g.p, eta.data(), reinterpret_cast<double*>(rho.data()), &ps), (std::size_t)ps.step);
+    if (stats) stats->rhst_transforms = ps.rhst_count;
+    manybeam::ComplexVector out(n);
+    for (int i = 0; i < n; ++i) out(i) = rho[(std::size_t)i];
+    return out;
+  });
 }
 
 }  // namespace manybeam::b200

@@ -9,6 +9,9 @@
 #include <limits>
 
 #include "manybeam/curve.hpp"
+#include "manybeam/geometry.hpp"
+#include "manybeam/proposed.hpp"
+#include "manybeam/slicing.hpp"
 #include "manybeam/sweep.hpp"
 #include "manybeam_b200_ref.hpp"
 #include "support/fields.hpp"
@@ -71,4 +74,32 @@ TEST_CASE("breakdown arrives as the reference's BreakdownError with a step") {
     caught = e.step > 0;
   }
   CHECK(caught);
+}
+
+TEST_CASE("the drop-in solve_proposed takes the reference's R_init") {
+  const RodSet rods = testfields::rods11();
+  const PotentialField field = testfields::layered_field();
+  const BoundPotential bound(field, rods);
+  const BeamGeometry beam(testfields::kGamma11, 7.0, 0.0);
+  const GammaMatrix gm = GammaMatrix::build(rods, beam);
+  const SlicingPlan plan = SlicingPlan::with_target_dz(field.z_bottom(), 0.02);
+  const int n = rods.size();
+  ComplexMatrix R(n, n);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) R(i, j) = Complex(0.03 * std::cos(1.0 + i + 2.0 * j), 0.02 * std::sin(0.5 + 3.0 * i - j));
+  for (const char* method : {"rk4", "sp4", "sp6"}) {
+    const StepperSpec& spec = StepperSpec::by_name(method);
+    SolveStats want_stats, got_stats;
+    const ComplexVector want = solve_proposed(bound, gm, plan, spec, {}, R, nullptr, &want_stats);
+    const ComplexVector got = b200::solve_proposed(field, rods, beam, plan, spec, {}, R, &got_stats);
+    CHECK(got_stats.rhst_transforms == want_stats.rhst_transforms);
+    CHECK((got - want).norm() <= 1e-10 * want.norm());
+    // an empty R_init is the unseeded solve
+    const ComplexVector w0 = solve_proposed(bound, gm, plan, spec);
+    const ComplexVector g0 = b200::solve_proposed(field, rods, beam, plan, spec);
+    CHECK((g0 - w0).norm() <= 1e-10 * w0.norm());
+    CHECK((want - w0).norm() > 1e-6 * w0.norm());
+  }
+  CHECK_THROWS_AS(b200::solve_proposed(field, rods, beam, plan, StepperSpec::sp6(), {}, ComplexMatrix(3, 3)),
+                  SolverError);
 }

@@ -218,6 +218,11 @@ struct Opts {
   std::size_t table_budget_bytes = (std::size_t)1 << 30;
   // custom splitting stepper (StepperSpec::splitting, proposed.hpp:35-36)
   std::optional<mb::StepperSpec> stepper;
+  // caller-supplied R_init of solve_proposed (proposed.hpp:98-102): r_count
+  // matrices of n x n (row-major); 1 = shared by all rows, rows = one per row.
+  // Passed as given instead of the bulk seed.
+  std::vector<cd> r_init;
+  long r_count = 0;
 };
 
 bool conventional(const Opts& o) { return !o.stepper && o.method == "conventional"; }
@@ -278,7 +283,12 @@ Rows solve_rows(const RefField& field, const mb::RodSet& rods, double gamma, con
     const mb::BeamGeometry beam(gamma, th0, th1);
     const mb::GammaMatrix gm = mb::GammaMatrix::build(rods, beam);
     mb::ComplexMatrix R_init;
-    if (bound.bulk_period())
+    if (o.r_count > 0) {
+      const cd* src = o.r_init.data() + (o.r_count == 1 ? 0 : (std::size_t)row * n * n);
+      R_init = mb::ComplexMatrix(n, n);
+      for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) R_init(i, j) = src[(std::size_t)i * n + j];
+    } else if (bound.bulk_period())
       R_init = spec ? mb::compute_bulk_reflection_proposed(bound, gm, o.dz, *spec, popts, mb::BulkOptions{})
                     : mb::compute_bulk_reflection_conventional(bound, gm, o.dz, mb::BulkOptions{});
     mb::SolveStats stats;
@@ -502,6 +512,12 @@ PYBIND11_MODULE(mb_ref, m) {
       .def_readwrite("rhst_threshold", &Opts::rhst_threshold)
       .def_readwrite("threads", &Opts::threads)
       .def_readwrite("table_budget_bytes", &Opts::table_budget_bytes)
+      .def("set_r_init",
+           [](Opts& o, py::array_t<cd, py::array::c_style | py::array::forcecast> R) {
+             if (R.ndim() != 2 && R.ndim() != 3) throw std::invalid_argument("R_init: (n, n) or (rows, n, n)");
+             o.r_count = R.ndim() == 2 ? 1 : (long)R.shape(0);
+             o.r_init.assign(R.data(), R.data() + R.size());
+           })
       .def("set_splitting",
            [](Opts& o, const std::string& name, const std::string& variant, std::vector<double> drift,
               std::vector<double> kick) {

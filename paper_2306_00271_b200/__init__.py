@@ -156,6 +156,9 @@ def lib():
         L.mb_plan_create.argtypes = [C.c_void_p, C.POINTER(_Rods), C.POINTER(_Field), C.c_int, C.c_double,
                                      C.POINTER(_Pair), C.c_long, C.POINTER(_Stepper), C.POINTER(_Options),
                                      C.POINTER(C.c_void_p)]
+        L.mb_plan_create_seeded.argtypes = [C.c_void_p, C.POINTER(_Rods), C.POINTER(_Field), C.c_int, C.c_double,
+                                            C.POINTER(_Pair), C.c_long, C.POINTER(_Stepper), C.POINTER(_Options),
+                                            C.c_void_p, C.c_long, C.POINTER(C.c_void_p)]
         L.mb_plan_execute.argtypes = [C.c_void_p, C.c_void_p]
         L.mb_plan_results.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.mb_plan_timing.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double),
@@ -506,9 +509,11 @@ def default_context():
 class Plan:
     """Batched solve over (structure, angle) pairs sharing rods, gamma and
     slicing: create (host prep + uploads) / execute (K1 + K2 on the device) /
-    results (D2H)."""
+    results (D2H). r_init: optional caller-supplied R_init of solve_proposed
+    (proposed.hpp:98-102), one (n, n) complex matrix shared by every pair or
+    (npairs, n, n); it replaces the bulk seed."""
 
-    def __init__(self, rods, fields, gamma, pairs, opts, ctx=None):
+    def __init__(self, rods, fields, gamma, pairs, opts, ctx=None, r_init=None):
         self.ctx = ctx or default_context()
         self.rods, self.fields = rods, list(fields)
         self.pairs = np.asarray(pairs)
@@ -520,8 +525,18 @@ class Plan:
         parr = (_Pair * len(self.pairs))(*[_Pair(int(s), float(t0), float(t1)) for s, t0, t1 in self.pairs])
         self._arrays = (farr, parr)
         self._h = C.c_void_p()
-        _check(lib().mb_plan_create(self.ctx._h, C.byref(crods), farr, len(cfields), float(gamma), parr,
-                                    len(self.pairs), C.byref(cst), C.byref(copt), C.byref(self._h)))
+        if r_init is None:
+            _check(lib().mb_plan_create(self.ctx._h, C.byref(crods), farr, len(cfields), float(gamma), parr,
+                                        len(self.pairs), C.byref(cst), C.byref(copt), C.byref(self._h)))
+        else:
+            R = np.ascontiguousarray(r_init, np.complex128)
+            if R.ndim == 2:
+                R = R[None]
+            if R.ndim != 3 or R.shape[1:] != (self.n, self.n):
+                raise SolverError("R_init has wrong dimensions")  # proposed.cpp:126
+            _check(lib().mb_plan_create_seeded(self.ctx._h, C.byref(crods), farr, len(cfields), float(gamma), parr,
+                                               len(self.pairs), C.byref(cst), C.byref(copt), _ptr(R), R.shape[0],
+                                               C.byref(self._h)))
         self.npairs = len(self.pairs)
 
     def execute(self, stream=None):
@@ -587,15 +602,24 @@ class Plan:
             pass
 
 
-def solve_batch(fields, rods, gamma, pairs, opts, ctx=None, want_rho=True):
+def solve_batch(fields, rods, gamma, pairs, opts, ctx=None, want_rho=True, r_init=None):
     """Batched structures: pairs = [(structure_index, theta0_deg, theta1_deg)].
     Returns (eta[npairs][n], rho, status)."""
-    plan = Plan(rods, fields, gamma, pairs, opts, ctx)
+    plan = Plan(rods, fields, gamma, pairs, opts, ctx, r_init=r_init)
     try:
         plan.execute()
         return plan.results(want_rho)
     finally:
         plan.close()
+
+
+def solve_proposed(field, rods, gamma, theta0_deg, theta1_deg, opts, r_init=None, ctx=None):
+    """solve_proposed (proposed.hpp:98-102, proposed.cpp:293-309) for one beam
+    direction: rho0, the first column of R at the surface, from the state
+    seeded with R_init (zero when None) at z_bottom. Returns (rho0, rhst_count);
+    breakdowns raise like the reference (BreakdownError with the step)."""
+    _, rho, st = solve_batch([field], rods, gamma, [(0, theta0_deg, theta1_deg)], opts, ctx, True, r_init)
+    return rho[0], int(st["rhst"][0])
 
 
 def rocking_curve(field, rods, gamma, grid, opts, ctx=None):

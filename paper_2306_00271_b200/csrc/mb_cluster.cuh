@@ -1239,8 +1239,39 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
   double* const Rr = BULK ? p.bulk_scratch + pair * 2 * NN : nullptr;  // previous R (row-major)
   double* const Ri = BULK ? Rr + NN : nullptr;
   bool again = false;  // BULK: another window follows
+  // the slab's initial state comes from R (Rr, Ri): the settled bulk R, or a
+  // caller-supplied R_init (p.r_seed; solve_proposed's R_init, proposed.cpp:301)
+  bool seed = BULK && p.r_seed != 0;
   do {
   again = false;
+  if (BULK && seed) {
+    // ---- seeded slab: Q = G^-1 (I + R) / 2, P = (i/2)(I - R) (proposed.cpp:114-128)
+    FOR_OWN {
+      const int r = orow(m);
+      const double2 gv = r < n ? p.ginv[pair * n + r] : make_double2(0.0, 0.0);
+      const long o = (long)r * NP + col0 + ocol(nb);
+      double2 rr = make_double2(0.0, 0.0), ri = rr;
+      if (r < n) {
+        rr = __ldcg(reinterpret_cast<const double2*>(Rr + o));
+        ri = __ldcg(reinterpret_cast<const double2*>(Ri + o));
+      }
+      double q0[4];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = col0 + ocol(nb) + e;
+        const double dlt = (r == c && r < n) ? 1.0 : 0.0;
+        const double re = (e ? rr.y : rr.x), im = (e ? ri.y : ri.x);
+        const double ar = 0.5 * (dlt + re), ai = 0.5 * im;  // (I + R) / 2
+        q0[e] = gv.x * ar - gv.y * ai;
+        q0[2 + e] = gv.x * ai + gv.y * ar;
+        P[m][nb][e] = 0.5 * im;  // (i/2)(I - R) = Im(R)/2 + i (1 - Re R)/2
+        P[m][nb][2 + e] = 0.5 * (dlt - re);
+      }
+      st(Ar, Ai, m, nb, q0);
+    }
+    __syncthreads();
+    seed = false;
+  }
   L = (BULK && bulk_phase) ? p.bulk_steps : p.nsteps;
   const double wh = (BULK && bulk_phase) ? p.bulk_h : p.h;
   const double wfin = (BULK && bulk_phase) ? p.bulk_final_drift : p.final_drift;
@@ -1668,31 +1699,8 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
       again = true;
       continue;
     }
-    // ---- seeded slab: Q = G^-1 (I + R) / 2, P = (i/2)(I - R) (proposed.cpp:114-128)
-    FOR_OWN {
-      const int r = orow(m);
-      const double2 gv = r < n ? p.ginv[pair * n + r] : make_double2(0.0, 0.0);
-      const long o = (long)r * NP + col0 + ocol(nb);
-      double2 rr = make_double2(0.0, 0.0), ri = rr;
-      if (r < n) {
-        rr = __ldcg(reinterpret_cast<const double2*>(Rr + o));
-        ri = __ldcg(reinterpret_cast<const double2*>(Ri + o));
-      }
-      double q0[4];
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int c = col0 + ocol(nb) + e;
-        const double dlt = (r == c && r < n) ? 1.0 : 0.0;
-        const double re = (e ? rr.y : rr.x), im = (e ? ri.y : ri.x);
-        const double ar = 0.5 * (dlt + re), ai = 0.5 * im;  // (I + R) / 2
-        q0[e] = gv.x * ar - gv.y * ai;
-        q0[2 + e] = gv.x * ai + gv.y * ar;
-        P[m][nb][e] = 0.5 * im;  // (i/2)(I - R) = Im(R)/2 + i (1 - Re R)/2
-        P[m][nb][2 + e] = 0.5 * (dlt - re);
-      }
-      st(Ar, Ai, m, nb, q0);
-    }
-    __syncthreads();
+    // settled: the slab starts from the seeded state (top of the loop)
+    seed = true;
     bulk_phase = false;
     period = 0;
     again = true;
@@ -1722,7 +1730,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
 template <class C, bool RK4, bool COOP>
 cudaError_t launch_one(const PropagateParams& p, cudaStream_t st, int cs, int* groups_out) {
   const Layout LY = cluster_layout(C::NP, C::SW, RK4 ? 3 : 2, p.box_size, p.ndiff);
-  auto kern = p.bulk_steps > 0 ? cluster_kernel<C, RK4, true, COOP> : cluster_kernel<C, RK4, false, COOP>;
+  auto kern = (p.bulk_steps > 0 || p.r_seed) ? cluster_kernel<C, RK4, true, COOP> : cluster_kernel<C, RK4, false, COOP>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LY.total);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};

@@ -490,10 +490,17 @@ void free_plan(mb_plan* pl) {
   delete pl;
 }
 
+// r_init (optional): caller-supplied R_init of solve_proposed (proposed.hpp:98-102),
+// r_count matrices of n x n complex (row-major, interleaved re/im); 1 = shared
+// by every pair, npairs = one per pair. It replaces the bulk seed.
 mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* fields, int nfields, double gamma,
-                     const mb_pair* pairs, long npairs, const mb_stepper* stepper, const mb_options* opts) {
+                     const mb_pair* pairs, long npairs, const mb_stepper* stepper, const mb_options* opts,
+                     const double* r_init = nullptr, long r_count = 0) {
   if (!ctx || !rods || !fields || !pairs || !stepper || !opts) fail(MB_ERR_ARG, "null argument");
   if (nfields < 1 || npairs < 1) fail(MB_ERR_ARG, "need at least one field and one pair");
+  if (r_init && r_count != 1 && r_count != npairs)
+    fail(MB_ERR_ARG, "R_init: count must be 1 (shared) or the number of pairs");
+  if (!r_init && r_count != 0) fail(MB_ERR_ARG, "R_init: null array with a nonzero count");
   const int n = rods->n, ndiff = rods->ndiff;
   if (n < 1 || ndiff < 1 || !rods->k || !rods->m || !rods->diff || !rods->diff_m || !rods->diff_index)
     fail(MB_ERR_ARG, "rods: empty or missing arrays");
@@ -516,13 +523,14 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
   if (conv && n > 32) fail(MB_ERR_CONFIG, "conventional method on the device supports at most 32 rods");
   if (conv && fields[0].has_bulk_period)
     fail(MB_ERR_CONFIG, "conventional method on the device: bulk seeding is not supported");
+  if (conv && r_init) fail(MB_ERR_CONFIG, "conventional method on the device: R_init is not supported");
   int npad = conv ? 0 : mbx::propagate_supported(n, stepper->algorithm == MB_STEP_RK4);
   if (conv && opts->path != 0) fail(MB_ERR_CONFIG, "conventional method: path must be 0");
   if (opts->path == 1 && !npad) fail(MB_ERR_CONFIG, "resident kernel does not cover this rod count / stepper");
   if (opts->path < 0 || opts->path > 4) fail(MB_ERR_ARG, "options: path must be 0..4");
   if (opts->path >= 2) npad = 0;
   if (conv) npad = 2 * n;
-  if (fields[0].has_bulk_period && opts->path == 2)
+  if (fields[0].has_bulk_period && !r_init && opts->path == 2)
     fail(MB_ERR_CONFIG, "bulk seeding runs in the resident and cluster kernels only (path 0, 1, 3 or 4)");
   bool big = npad == 0 && !conv;
   if (big) npad = (n + 7) & ~7;
@@ -560,7 +568,9 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
   // bulk window (proposed.cpp:311-321): one period below z_bottom, in
   // max(1, round(period / dz)) steps of StepWindow::over(zb - p, zb, .); the
   // potential there is the periodic continuation (map_z)
-  const bool bulk = fields[0].has_bulk_period != 0;
+  // (a caller-supplied R_init replaces the bulk seed: solve_proposed takes
+  // R_init as given, proposed.cpp:301)
+  const bool bulk = fields[0].has_bulk_period != 0 && !r_init;
   long Lb = 0;
   double hb = 0.0;
   if (bulk) {
@@ -823,6 +833,23 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
       p.bulk_tol = 1e-12;
       p.bulk_scratch = dev_alloc<double>(pl, (std::size_t)npairs * 2 * npad * npad);
     }
+    p.r_seed = 0;
+    if (r_init) {  // zero-padded re / im planes per pair (ld npad), read by every design
+      const std::size_t NN = (std::size_t)npad * npad;
+      std::vector<double> planes((std::size_t)npairs * 2 * NN, 0.0);
+      for (long q = 0; q < npairs; ++q) {
+        const double* src = r_init + (r_count == 1 ? 0 : (std::size_t)q * 2 * n * n);
+        double* re = planes.data() + (std::size_t)q * 2 * NN;
+        double* im = re + NN;
+        for (int i = 0; i < n; ++i)
+          for (int j = 0; j < n; ++j) {
+            re[(std::size_t)i * npad + j] = src[2 * ((std::size_t)i * n + j)];
+            im[(std::size_t)i * npad + j] = src[2 * ((std::size_t)i * n + j) + 1];
+          }
+      }
+      p.bulk_scratch = dev_upload(pl, planes.data(), planes.size());
+      p.r_seed = 1;
+    }
     p.eta = dev_alloc<double>(pl, (std::size_t)npairs * n);
     p.rho = dev_alloc<double2>(pl, (std::size_t)npairs * n);
     p.status = dev_alloc<mbx::PointStatus>(pl, (std::size_t)npairs);
@@ -837,7 +864,7 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
     pl->stride = (int)stride;
     // cluster kernel: A, B, panel rows (+ the saved Q slab of a bulk period)
     if (cluster) {
-      p.scratch = dev_alloc<double>(pl, (std::size_t)npairs * (bulk ? 8 : 6) * npad * npad);
+      p.scratch = dev_alloc<double>(pl, (std::size_t)npairs * ((bulk || r_init) ? 8 : 6) * npad * npad);
       // cluster or cooperative groups: path 3 / 4 force one; auto takes the
       // variant that finishes the batch in fewer rounds of co-resident groups
       p.coop = opts->path == 4 ? 1 : (opts->path == 3 ? 0 : mbx::cluster_prefer_coop(p));
@@ -868,6 +895,7 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
       b.gdiag = p.gdiag;
       b.ginv = p.ginv;
       b.sin_theta0 = p.sin_theta0;
+      b.r_init = r_init ? p.bulk_scratch : nullptr;
       // splitting: Q0, Q1 (ping-pong), P, scratch; rk4: Q, P, X2, X3, W, V, SQ
       b.nmat = p.rk4 ? 7 : 4;
       b.pair_stride = (long)b.nmat * 2 * npad * npad;
@@ -1104,7 +1132,8 @@ int collect_results(mb_plan* pl, double* eta, double* rho, mb_point_status* stat
 // structure's coefficient table is built on one device only). One field:
 // pairs round-robin. Fixed map, so the gathered rows do not depend on timing.
 mb_plan* create_multi_plan(mb_context* ctx, const mb_rods* rods, const mb_field* fields, int nfields, double gamma,
-                           const mb_pair* pairs, long npairs, const mb_stepper* stepper, const mb_options* opts) {
+                           const mb_pair* pairs, long npairs, const mb_stepper* stepper, const mb_options* opts,
+                           const double* r_init, long r_count) {
   if (!pairs || !fields) fail(MB_ERR_ARG, "null argument");
   if (nfields < 1 || npairs < 1) fail(MB_ERR_ARG, "need at least one field and one pair");
   const int G = (int)ctx->subs.size();
@@ -1156,8 +1185,22 @@ mb_plan* create_multi_plan(mb_context* ctx, const mb_rods* rods, const mb_field*
           rows.push_back(p);
         }
       if (mine.empty()) continue;
+      // per-pair R_init follows its pair to the owning device
+      std::vector<double> seed;
+      const double* r_mine = r_init;
+      long r_mine_count = r_count;
+      if (r_init && r_count != 1) {
+        if (r_count != npairs || !rods) fail(MB_ERR_ARG, "R_init: count must be 1 (shared) or the number of pairs");
+        const std::size_t per = (std::size_t)2 * rods->n * rods->n;
+        seed.resize(rows.size() * per);
+        for (std::size_t q = 0; q < rows.size(); ++q)
+          std::memcpy(seed.data() + q * per, r_init + (std::size_t)rows[q] * per, per * sizeof(double));
+        r_mine = seed.data();
+        r_mine_count = (long)rows.size();
+      }
       mb_plan* sp = create_plan(ctx->subs[(std::size_t)g], rods, fields + s_lo[g], s_hi[g] - s_lo[g], gamma,
-                                mine.data(), (long)mine.size(), stepper, opts);
+                                mine.data(), (long)mine.size(), stepper, opts, r_mine, r_mine_count);
+      // (the pageable upload is staged before create_plan returns)
       pl->shards.push_back(sp);
       pl->shard_rows.push_back(std::move(rows));
       pl->shard_s0.push_back(s_lo[g]);
@@ -1215,10 +1258,12 @@ void destroy_any(mb_plan* pl) {
 }
 
 mb_plan* create_any(mb_context* ctx, const mb_rods* rods, const mb_field* fields, int nfields, double gamma,
-                    const mb_pair* pairs, long npairs, const mb_stepper* stepper, const mb_options* opts) {
+                    const mb_pair* pairs, long npairs, const mb_stepper* stepper, const mb_options* opts,
+                    const double* r_init = nullptr, long r_count = 0) {
   if (!ctx) fail(MB_ERR_ARG, "null context");
-  if (!ctx->subs.empty()) return create_multi_plan(ctx, rods, fields, nfields, gamma, pairs, npairs, stepper, opts);
-  mb_plan* pl = create_plan(ctx, rods, fields, nfields, gamma, pairs, npairs, stepper, opts);
+  if (!ctx->subs.empty())
+    return create_multi_plan(ctx, rods, fields, nfields, gamma, pairs, npairs, stepper, opts, r_init, r_count);
+  mb_plan* pl = create_plan(ctx, rods, fields, nfields, gamma, pairs, npairs, stepper, opts, r_init, r_count);
   cuda_check(cudaStreamSynchronize(ctx->stream), "plan upload");
   return pl;
 }
@@ -1386,6 +1431,17 @@ int mb_plan_create(mb_context* ctx, const mb_rods* rods, const mb_field* fields,
     *out = nullptr;
     std::lock_guard<std::mutex> lk(ctx->mu);
     *out = create_any(ctx, rods, fields, nfields, gamma, pairs, npairs, stepper, opts);
+  });
+}
+
+int mb_plan_create_seeded(mb_context* ctx, const mb_rods* rods, const mb_field* fields, int nfields, double gamma,
+                          const mb_pair* pairs, long npairs, const mb_stepper* stepper, const mb_options* opts,
+                          const double* r_init, long r_init_count, mb_plan** out) {
+  return guarded([&] {
+    if (!out || !ctx) fail(MB_ERR_ARG, "null argument");
+    *out = nullptr;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    *out = create_any(ctx, rods, fields, nfields, gamma, pairs, npairs, stepper, opts, r_init, r_init_count);
   });
 }
 

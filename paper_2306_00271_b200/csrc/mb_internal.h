@@ -86,6 +86,11 @@ struct PropagateParams {
   long bulk_max_periods;
   double bulk_tol;
   double* bulk_scratch;       // per pair 2 NP^2 doubles: the previous period's R
+  // caller-supplied R_init (solve_proposed's R_init, proposed.hpp:98-102,
+  // initial_state proposed.cpp:123-128): bulk_scratch holds it per pair as
+  // zero-padded re / im planes (row-major, ld NP) and the slab starts from
+  // Q = G^-1 (I + R)/2, P = (i/2)(I - R); no bulk window runs
+  int r_seed;
   // cluster kernel, cooperative variant (COOP): persistent groups of coop_cs
   // co-resident CTAs exchanging through L2 instead of DSMEM
   int coop;                   // 1: cooperative grid, 0: one thread-block cluster per pair
@@ -128,6 +133,7 @@ struct BigParams {
   int residual_check;
   double* eta;
   double2* rho;
+  const double* r_init;  // caller-supplied R_init per pair (2 np^2 doubles: re, im planes) or null
 };
 
 // one tiled-GEMM launch: acc = U(slot) * M[op]; epilogue `kind`

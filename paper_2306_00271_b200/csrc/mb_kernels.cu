@@ -731,7 +731,37 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
   long period = 0;
   double* const Rr = BULK ? p.bulk_scratch + pair * 2 * NP * NP : nullptr;  // previous R
   double* const Ri = BULK ? Rr + NP * NP : nullptr;
+  // the slab's initial state comes from R (Rr, Ri): the settled bulk R, or a
+  // caller-supplied R_init (p.r_seed; solve_proposed's R_init, proposed.cpp:301)
+  bool seed = BULK && p.r_seed != 0;
   for (;;) {
+  if (BULK && seed) {
+    // ---- seeded slab: Q = G^-1 (I + R) / 2, P = (i/2)(I - R) (proposed.cpp:114-128)
+    FOR_BLK {
+      const int r = own.r(mb);
+      const double2 gi = r < n ? p.ginv[pair * n + r] : make_double2(0.0, 0.0);
+      const int o = r * NP + own.c(nb);
+      const double2 rr = *reinterpret_cast<const double2*>(Rr + o);
+      const double2 ri = *reinterpret_cast<const double2*>(Ri + o);
+      double q0[4];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = own.c(nb) + e;
+        const double dlt = (r == c && r < n) ? 1.0 : 0.0;
+        const double re = (e ? rr.y : rr.x), im = (e ? ri.y : ri.x);
+        const double ar = 0.5 * (dlt + re), ai = 0.5 * im;  // (I + R) / 2
+        q0[e] = gi.x * ar - gi.y * ai;
+        q0[2 + e] = gi.x * ai + gi.y * ar;
+        P[mb][nb][e] = 0.5 * im;  // (i/2)(I - R) = Im(R)/2 + i (1 - Re R)/2
+        P[mb][nb][2 + e] = 0.5 * (dlt - re);
+      }
+      own.st(Ar, Ai, mb, nb, q0);
+    }
+    __syncthreads();
+    rebuild_sum();
+    __syncthreads();
+    seed = false;
+  }
   const bool main = !bulk_phase;
   const int L = WL();
   const int step_off = (int)(period * L);
@@ -1129,30 +1159,8 @@ __global__ void __launch_bounds__(C::NT, C::MINB) propagate_kernel(const __grid_
       continue;
     }
   }
-  // ---- seeded slab: Q = G^-1 (I + R) / 2, P = (i/2)(I - R) (proposed.cpp:114-128)
-  FOR_BLK {
-    const int r = own.r(mb);
-    const double2 gi = r < n ? p.ginv[pair * n + r] : make_double2(0.0, 0.0);
-    const int o = r * NP + own.c(nb);
-    const double2 rr = *reinterpret_cast<const double2*>(Rr + o);
-    const double2 ri = *reinterpret_cast<const double2*>(Ri + o);
-    double q0[4];
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int c = own.c(nb) + e;
-      const double dlt = (r == c && r < n) ? 1.0 : 0.0;
-      const double re = (e ? rr.y : rr.x), im = (e ? ri.y : ri.x);
-      const double ar = 0.5 * (dlt + re), ai = 0.5 * im;  // (I + R) / 2
-      q0[e] = gi.x * ar - gi.y * ai;
-      q0[2 + e] = gi.x * ai + gi.y * ar;
-      P[mb][nb][e] = 0.5 * im;  // (i/2)(I - R) = Im(R)/2 + i (1 - Re R)/2
-      P[mb][nb][2 + e] = 0.5 * (dlt - re);
-    }
-    own.st(Ar, Ai, mb, nb, q0);
-  }
-  __syncthreads();
-  rebuild_sum();
-  __syncthreads();
+  // settled: the slab starts from the seeded state (top of the loop)
+  seed = true;
   bulk_phase = false;
   period = 0;
   }
@@ -1190,7 +1198,7 @@ static size_t smem_bytes(const PropagateParams& p) {
 template <class C, bool RK4>
 static cudaError_t launch_cfg(const PropagateParams& p, cudaStream_t st) {
   const size_t smem = smem_bytes<C, RK4>(p);
-  auto kern = p.bulk_steps > 0 ? propagate_kernel<C, RK4, true> : propagate_kernel<C, RK4, false>;
+  auto kern = (p.bulk_steps > 0 || p.r_seed) ? propagate_kernel<C, RK4, true> : propagate_kernel<C, RK4, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   kern<<<(unsigned)p.npairs, C::NT, smem, st>>>(p);

@@ -346,9 +346,23 @@ __global__ void big_elem_kernel(const __grid_constant__ BigParams p, const __gri
         p.xi[pair] = 0.0;
       }
       const bool d = (r == c) && (r < p.n);
-      const double2 gi = d ? p.ginv[pair * p.n + r] : make_double2(0.0, 0.0);
-      const double qr = d ? 0.5 * gi.x : 0.0, qi = d ? 0.5 * gi.y : 0.0;
-      const double pr = 0.0, pi = d ? 0.5 : 0.0;
+      double qr, qi, pr, pi;
+      if (p.r_init) {
+        // caller-supplied R_init: Q = G^-1 (I + R)/2, P = (i/2)(I - R)
+        // (from_tau_rho, proposed.cpp:114-128; the on-chip kernels' seeded slab)
+        const double2 gi = r < p.n ? p.ginv[pair * p.n + r] : make_double2(0.0, 0.0);
+        const double re = p.r_init[pair * 2 * NN + o], im = p.r_init[pair * 2 * NN + NN + o];
+        const double dlt = d ? 1.0 : 0.0;
+        const double ar = 0.5 * (dlt + re), ai = 0.5 * im;
+        qr = gi.x * ar - gi.y * ai;
+        qi = gi.x * ai + gi.y * ar;
+        pr = 0.5 * im;
+        pi = 0.5 * (dlt - re);
+      } else {
+        const double2 gi = d ? p.ginv[pair * p.n + r] : make_double2(0.0, 0.0);
+        qr = d ? 0.5 * gi.x : 0.0, qi = d ? 0.5 * gi.y : 0.0;
+        pr = 0.0, pi = d ? 0.5 : 0.0;
+      }
       double* Q = mat(p, pair, s.mq);
       double* P = mat(p, pair, s.mp);
       Q[o] = qr;

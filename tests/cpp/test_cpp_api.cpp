@@ -116,6 +116,24 @@ int main(int argc, char** argv) {
     }
     CHECK(broke);
     CHECK_THROWS_AS(rocking_curve(field, rods, 2.5, grid, SweepOptions{"sp8"}), ConfigError);
+    {  // solve_proposed with R_init (proposed.hpp:98-102): zero R_init = the sweep's row
+      SolveStats stats;
+      const std::vector<Complex> rho0 = solve_proposed(field, rods, 2.5, 8.0, 0.0, o, {}, &stats);
+      const std::vector<Complex> zero((std::size_t)(rods.size() * rods.size()), Complex(0.0, 0.0));
+      const std::vector<Complex> rhoz = solve_proposed(field, rods, 2.5, 8.0, 0.0, o, zero);
+      double d = 0.0, dz = 0.0;
+      for (int i = 0; i < rods.size(); ++i) {
+        d = std::max(d, std::abs(rho0[(std::size_t)i] - a.rho[(std::size_t)(1 * a.rods + i)]));
+        dz = std::max(dz, std::abs(rhoz[(std::size_t)i] - rho0[(std::size_t)i]));
+      }
+      CHECK(d == 0.0 && dz == 0.0);
+      CHECK(stats.rhst_transforms == a.status[1].rhst_count);
+      std::vector<Complex> seeded = zero;
+      for (int i = 0; i < rods.size(); ++i) seeded[(std::size_t)(i * rods.size() + i)] = Complex(0.2, -0.1);
+      const std::vector<Complex> rhos = solve_proposed(field, rods, 2.5, 8.0, 0.0, o, seeded);
+      CHECK(std::abs(rhos[0] - rho0[0]) > 1e-6);  // the substrate reflection reaches the surface
+      CHECK_THROWS_AS(solve_proposed(field, rods, 2.5, 8.0, 0.0, o, std::vector<Complex>(5)), SolverError);
+    }
   }
   std::printf("%s: %d failure(s)\n", device ? "device" : "host-only", failures);
   return failures;

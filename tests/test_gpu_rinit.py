@@ -1,0 +1,138 @@
+"""Caller-supplied R_init (solve_proposed's R_init, proposed.hpp:98-102;
+initial_state, proposed.cpp:123-128) through mb_plan_create_seeded on every
+design — resident, thread-block clusters, cooperative groups, batched —
+against the reference build (oracle/_ref, fixture `ref`) running
+solve_proposed with the same R_init. Tolerance: the parity gate of
+test_gpu_parity.py (curve_error and per-entry 1e-9 above 1e-12 max eta)."""
+import numpy as np
+import pytest
+
+import fields as F
+import harness as H
+import paper_2306_00271_b200 as mb
+from paper_2306_00271_b200 import configs
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-9
+
+
+def seeded_r(n, count, seed=7, scale=0.4):
+    """|R| well below 1 (a reflecting substrate), dense and complex."""
+    rng = np.random.default_rng(seed)
+    R = rng.standard_normal((count, n, n)) + 1j * rng.standard_normal((count, n, n))
+    return scale * R / n
+
+
+def ref_rows(ref, field, rods, gamma, t0, method, dz, R, slices=0):
+    opts = ref.SweepOptions()
+    opts.method, opts.dz, opts.threads, opts.slices = method, dz, 4, slices
+    opts.set_r_init(R)
+    return ref.rocking_curve(field, rods, gamma, ref.AngleGrid.validated(list(t0), [0.0]), opts)
+
+
+@pytest.mark.parametrize("method", ["rk4", "sp4", "sp6"])
+@pytest.mark.parametrize("shared", [True, False])
+def test_r_init_resident_parity(ref, method, shared):
+    t0 = [2.0, 7.0, 15.0, 25.0]
+    n = F.rods11(ref).size()
+    R = seeded_r(n, 1 if shared else len(t0))
+    rc = ref_rows(ref, F.layered_field(ref), F.rods11(ref), F.K_GAMMA11, t0, method, 0.02, R[0] if shared else R)
+    field = mb.PotentialField.gaussian_layers(-10.0, F.LAYERED_LAYERS)
+    rods = mb.RodSet.build(mb.Lattice2D(*F.RECT), 5.0)
+    eta, rho, st = mb.solve_batch([field], rods, F.K_GAMMA11, [(0, t, 0.0) for t in t0],
+                                  mb.SweepOptions(method=method, dz=0.02), r_init=R[0] if shared else R)
+    assert np.array_equal(st["rhst"], rc.rhst)
+    assert H.curve_err(eta, rc.eta) <= TOL
+    assert H.entry_rel_err(eta, rc.eta) <= TOL
+    assert np.abs(rho - rc.rho).max() <= 1e-10 * np.abs(rc.rho).max()
+
+
+def test_r_init_replaces_bulk_seed(ref):
+    """solve_proposed takes R_init as given (proposed.cpp:301): a field with a
+    bulk period is not solved for its bulk R when the caller supplies one."""
+    t0 = [2.0, 7.0]
+    n = F.rods11(ref).size()
+    R = seeded_r(n, 1)[0]
+    of = ref.PotentialField.gaussian_layers(-10.0, F.LAYERED_LAYERS, 5.0)
+    rc = ref_rows(ref, of, F.rods11(ref), F.K_GAMMA11, t0, "sp6", 0.05, R)
+    field = mb.PotentialField.gaussian_layers(-10.0, F.LAYERED_LAYERS, bulk_period=5.0)
+    rods = mb.RodSet.build(mb.Lattice2D(*F.RECT), 5.0)
+    eta, _, st = mb.solve_batch([field], rods, F.K_GAMMA11, [(0, t, 0.0) for t in t0],
+                                mb.SweepOptions(method="sp6", dz=0.05), r_init=R)
+    assert np.array_equal(st["rhst"], rc.rhst)
+    assert H.curve_err(eta, rc.eta) <= TOL and H.entry_rel_err(eta, rc.eta) <= TOL
+
+
+def test_zero_r_init_is_the_unseeded_solve():
+    """A zero R_init is the unseeded solve (initial_state with R = 0)."""
+    t0 = [2.0, 9.0]
+    field = mb.PotentialField.gaussian_layers(-10.0, F.LAYERED_LAYERS)
+    rods = mb.RodSet.build(mb.Lattice2D(*F.RECT), 5.0)
+    opts = mb.SweepOptions(method="sp6", dz=0.02)
+    pairs = [(0, t, 0.0) for t in t0]
+    a, _, _ = mb.solve_batch([field], rods, F.K_GAMMA11, pairs, opts)
+    b, _, _ = mb.solve_batch([field], rods, F.K_GAMMA11, pairs, opts, r_init=np.zeros((rods.size(), rods.size()), complex))
+    assert np.array_equal(a, b)
+
+
+def large_case(n_rods, method):
+    w = configs.config4(n_rods, method, n_structures=1).subset(theta0=[0.8, 2.3, 4.1], slices=40, z_bottom=-0.64)
+    return w
+
+
+@pytest.mark.parametrize("n_rods,method,path", [(81, "sp6", 3), (81, "sp6", 4), (81, "sp6", 2), (127, "rk4", 3),
+                                                (127, "rk4", 2), (255, "sp6", 4), (255, "rk4", 2)])
+def test_r_init_large_designs_parity(ref, oracle, n_rods, method, path):
+    w = large_case(n_rods, method)
+    R = seeded_r(n_rods, len(w.theta0), seed=11)
+    rods_r = ref.RodSet.build_first(H.oracle_lattice(ref, w), w.n_rods)
+    rc = ref_rows(ref, H.oracle_fields(ref, w)[0], rods_r, w.gamma, w.theta0, method, -w.z_bottom / w.slices, R,
+                  slices=w.slices)
+    rods = mb.RodSet.build_first(mb.Lattice2D(w.a1, w.a2), w.n_rods)
+    opts = mb.SweepOptions(method=method, slices=w.slices, dz=-w.z_bottom / w.slices, path=path)
+    eta, _, st = mb.solve_batch(configs.product_fields(w), rods, w.gamma, [(0, t, 0.0) for t in w.theta0], opts,
+                                r_init=R)
+    assert (st["code"] == 0).all()
+    assert np.array_equal(st["rhst"], rc.rhst)
+    assert H.curve_err(eta, rc.eta) <= TOL
+    assert H.entry_rel_err(eta, rc.eta) <= TOL
+
+
+def test_r_init_two_shards_equal_one_device():
+    """Per-pair R_init follows its pair through the multi-device gather."""
+    t0 = [2.0, 5.0, 9.0, 14.0, 20.0]
+    field = mb.PotentialField.gaussian_layers(-10.0, F.LAYERED_LAYERS)
+    rods = mb.RodSet.build(mb.Lattice2D(*F.RECT), 5.0)
+    R = seeded_r(rods.size(), len(t0), seed=3)
+    opts = mb.SweepOptions(method="sp6", dz=0.02)
+    pairs = [(0, t, 0.0) for t in t0]
+    one, _, _ = mb.solve_batch([field], rods, F.K_GAMMA11, pairs, opts, r_init=R)
+    ctx = mb.Context(devices=[0, 0])
+    try:
+        two, _, _ = mb.solve_batch([field], rods, F.K_GAMMA11, pairs, opts, ctx=ctx, r_init=R)
+    finally:
+        ctx.close()
+    assert np.array_equal(one, two)
+
+
+def test_solve_proposed_mirror(ref):
+    n = F.rods11(ref).size()
+    R = seeded_r(n, 1, seed=5)[0]
+    rc = ref_rows(ref, F.layered_field(ref), F.rods11(ref), F.K_GAMMA11, [7.0], "sp6", 0.02, R)
+    field = mb.PotentialField.gaussian_layers(-10.0, F.LAYERED_LAYERS)
+    rods = mb.RodSet.build(mb.Lattice2D(*F.RECT), 5.0)
+    rho0, rhst = mb.solve_proposed(field, rods, F.K_GAMMA11, 7.0, 0.0, mb.SweepOptions(method="sp6", dz=0.02), R)
+    assert rhst == rc.rhst[0]
+    assert np.abs(rho0 - rc.rho[0]).max() <= 1e-10 * np.abs(rc.rho[0]).max()
+
+
+def test_r_init_wrong_dimensions():
+    field = mb.PotentialField.gaussian_layers(-10.0, F.LAYERED_LAYERS)
+    rods = mb.RodSet.build(mb.Lattice2D(*F.RECT), 5.0)
+    opts = mb.SweepOptions(method="sp6", dz=0.02)
+    n = rods.size()
+    with pytest.raises(mb.SolverError):  # "R_init has wrong dimensions" (proposed.cpp:126)
+        mb.solve_batch([field], rods, F.K_GAMMA11, [(0, 5.0, 0.0)], opts, r_init=np.zeros((n + 1, n + 1), complex))
+    with pytest.raises(mb.Error):  # count neither 1 nor npairs
+        mb.solve_batch([field], rods, F.K_GAMMA11, [(0, 5.0, 0.0), (0, 6.0, 0.0), (0, 7.0, 0.0)], opts,
+                       r_init=np.zeros((2, n, n), complex))
