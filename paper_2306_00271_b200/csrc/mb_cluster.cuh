@@ -770,6 +770,134 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
     int* ptp = reinterpret_cast<int*>(tpub + 2 * SW);     // [16] pivot columns
     double2* ptinv = tpub;                                // [16] 1/pivot
     double* ptpv = reinterpret_cast<double*>(tpub + SW);  // [16] |pivot|^2
+    // ---- diagonal-pivot fast path. Measured at cfg3: 99.8% of all pivots
+    // are the diagonal (the first maximum of row k over j >= k is j = k), so
+    // the panel is first factorised WITHOUT the per-step row search and the
+    // pivot rule is verified afterwards; any violation (a strictly larger
+    // |A[k][j]|, j > k, or a pivot that is not > 0) discards the result and
+    // the chain below runs on the untouched rows.
+    //  (1) warp 0 eliminates the 16 x 16 diagonal block D alone (lane = row
+    //      r + 16 h holds columns 8h..8h+7 of row r): per step row k goes
+    //      through shared memory, x_{r,k} = D[r][k] / D[k][k] with the chain's
+    //      reciprocal, op k on the rows r > k; gives x, 1/pivot, |pivot|^2;
+    //  (2) every thread takes one column j outside D and applies the same
+    //      16 ops to it (X[r][j] -= x_{r,k} X[k][j], k < r: the arithmetic of
+    //      gj_rows in the same order), checks |X[k][j]|^2 <= |pivot_k|^2 for
+    //      the candidate columns j > k and writes the rows F_k straight to the
+    //      published area (L2).
+    bool fast = false;
+    if constexpr (SW == 16) {
+      double2* const xs = reinterpret_cast<double2*>(wchr);  // [k][r] x_{r,k}
+      double2* const rowb = xs + SW * SW;                     // [2][SW] row k of D
+      double2* const finv = rowb + 2 * SW;                    // [SW] 1/pivot
+      double* const fpv = reinterpret_cast<double*>(finv + SW);  // [SW] |pivot|^2
+      int viol = 0;
+      if (warp == 0 && nk > 0) {
+        const int r = lane & 15, h = lane >> 4;
+        double2 d[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int j = col0 + 8 * h + i;
+          d[i] = make_double2(Ar_[sw<NP>(r, j)], Ai_[sw<NP>(r, j)]);
+        }
+#pragma unroll
+        for (int k = 0; k < SW; ++k) {
+          if (k < nk) {
+            double2* const rb = rowb + (k & 1) * SW;
+            if (r == k) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) rb[8 * h + i] = d[i];
+            }
+            __syncwarp();
+            double2 f[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) f[i] = rb[8 * h + i];
+            const double2 akk = rb[k];
+            const double pv = akk.x * akk.x + akk.y * akk.y;
+            if (!(pv > 0.0)) viol = 1;  // zero / NaN pivot: the chain decides
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int c = 8 * h + i;
+              if (c > k && col0 + c < n && f[i].x * f[i].x + f[i].y * f[i].y > pv) viol = 1;
+            }
+            double rr;  // 1/|pivot|^2 as in gj_pivot
+#ifdef MB_EXACT_RCP
+            rr = 1.0 / pv;
+#else
+            asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rr) : "d"(pv));
+            rr = rr * fma(-pv, rr, 2.0);
+            rr = rr * fma(-pv, rr, 2.0);
+#endif
+            const double2 inv = pv > 0.0 ? make_double2(akk.x * rr, -akk.y * rr) : make_double2(0.0, 0.0);
+            const int src = r | ((k >> 3) << 4);  // the lane holding D[r][k]
+            const double2 drk = make_double2(__shfl_sync(0xffffffffu, d[k & 7].x, src),
+                                             __shfl_sync(0xffffffffu, d[k & 7].y, src));
+            const double2 x = cmul(drk, inv);
+            if (r > k) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const double2 v = d[i];
+                const double2 nv =
+                    make_double2(v.x - (f[i].x * x.x - f[i].y * x.y), v.y - (f[i].x * x.y + f[i].y * x.x));
+                d[i] = (8 * h + i == k) ? x : nv;
+              }
+              if (h == 0) xs[k * SW + r] = x;
+            }
+            if (lane == 0) {
+              finv[k] = inv;
+              fpv[k] = pv;
+            }
+          }
+        }
+        // row r of D after ops < r is final: its F entries and the table
+        if (r < nk) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const long o = (long)(col0 + r) * NP + col0 + 8 * h + i;
+            M2r[o] = d[i].x;
+            M2i[o] = d[i].y;
+          }
+        }
+        __syncwarp();
+        if (lane < nk) {
+          ptp[lane] = col0 + lane;
+          ptinv[lane] = finv[lane];
+          ptpv[lane] = fpv[lane];
+        }
+      }
+      __syncthreads();
+      CPROF(6);
+      for (int j = tid; j < NP; j += CNT) {
+        if (j >= col0 && j < col0 + SW) continue;
+        double2 X[SW];
+#pragma unroll
+        for (int r = 0; r < SW; ++r) X[r] = make_double2(Ar_[sw<NP>(r, j)], Ai_[sw<NP>(r, j)]);
+#pragma unroll
+        for (int k = 0; k < SW - 1; ++k) {
+          if (k < nk) {
+            const double2 f = X[k];
+#pragma unroll
+            for (int r = k + 1; r < SW; ++r) {
+              const double2 x = xs[k * SW + r];
+              X[r] = make_double2(X[r].x - (f.x * x.x - f.y * x.y), X[r].y - (f.x * x.y + f.y * x.x));
+            }
+          }
+        }
+        const bool cand = j >= col0 + SW && j < n;  // columns j > k of every panel row
+#pragma unroll
+        for (int k = 0; k < SW; ++k) {
+          if (k < nk) {
+            if (cand && X[k].x * X[k].x + X[k].y * X[k].y > fpv[k]) viol = 1;
+            const long o = (long)(col0 + k) * NP + j;
+            M2r[o] = X[k].x;
+            M2i[o] = X[k].y;
+          }
+        }
+      }
+      fast = nk > 0 && __syncthreads_or(viol) == 0;
+      CPROF(8);
+    }
+    if (!fast) {
     if (warp == 0 && nk > 0) {
       double2 a[NQ];
 #pragma unroll
@@ -792,11 +920,17 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
       double2 fj[NQ];
 #pragma unroll
       for (int q = 0; q < NQ; ++q) fj[q] = fpub[slot * NP + lane + 32 * q];
+#ifdef MB_PROFILE_FACTOR
+      CPROF(12);
+#endif
       if (warp == 0 && lk + 1 < nk) {  // chain: row k+1, then its pivot
         const int rows[1] = {lk + 1};
         const bool isA[1] = {true};
         double2 row[1][NQ];
         gj_rows<C, 1>(Ar_, Ai_, Br_, Bi_, rows, isA, k, piv, inv, fj, row, lane);
+#ifdef MB_PROFILE_FACTOR
+        CPROF(15);
+#endif
         gj_pivot<C>(row[0], k + 1, n, fpub + (slot ^ 1) * NP, *sc, slot ^ 1, lane);
       }
       CPROF(6);  // (thread 0 = warp 0: the pivot chain of the step)
@@ -807,6 +941,9 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
         gj_rows<C, 1>(Ar_, Ai_, Br_, Bi_, rows, isA, k, piv, inv, fj, row, lane);
       }
       __syncthreads();
+#ifdef MB_PROFILE_FACTOR
+      CPROF(3);
+#endif
     }
     CPROF(8);
     // publish the panel rows (F) to L2 for the consumers
@@ -817,6 +954,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
       *reinterpret_cast<double2*>(M2r + o) = *reinterpret_cast<const double2*>(Ar_ + so);
       *reinterpret_cast<double2*>(M2i + o) = *reinterpret_cast<const double2*>(Ai_ + so);
     }
+    }  // !fast
     __syncthreads();
     if (tid == 0) {
       __threadfence();  // tables and rows visible cluster-wide before the flag
