@@ -604,29 +604,31 @@ __global__ void __launch_bounds__(NTH, NPM == 128 ? 2 : 1) big_gj_kernel(const _
     int myfail = 0;
     for (int t = 0; t < bs; ++t) {
       const int ct = k0 + t, buf = t & 1;
-      if (c == ct) {
-        const double2 pv = make_double2(g.rr[swg(t, c)], g.ri[swg(t, c)]);
+      // the pivot column's scaling runs on the whole warp of thread ct (lane
+      // = row i of R, lane + 16 = row i of M) instead of one thread's 16-row loop
+      if ((ct >> 5) == warp) {
+        const double2 pv = make_double2(g.rr[swg(t, ct)], g.ri[swg(t, ct)]);
         const double m2 = pv.x * pv.x + pv.y * pv.y;
-        if (g.used[c] || !(m2 > 0.0)) myfail = 1;
-        if (!g.used[c]) {
-          g.used[c] = 1;
-          marked = true;
+        if (c == ct) {
+          if (g.used[c] || !(m2 > 0.0)) myfail = 1;
+          if (!g.used[c]) {
+            g.used[c] = 1;
+            marked = true;
+          }
+          g.inpanel[c] = 1;
+          g.pc[k0 + t] = c;
+          g.pv2[buf] = m2;
+          g.mr[swg(t, c)] = 1.0;  // row c of E is e_c until now
         }
-        g.inpanel[c] = 1;
-        g.pc[k0 + t] = c;
-        g.pv2[buf] = m2;
-        g.mr[swg(t, c)] = 1.0;  // row c of E is e_c until now
+        __syncwarp();
         const double2 inv = cinv(pv);
-        for (int i = 0; i < GB; ++i) {
-          const double2 x = cmul(make_double2(g.rr[swg(i, c)], g.ri[swg(i, c)]), inv);
-          const double2 y = cmul(make_double2(g.mr[swg(i, c)], g.mi[swg(i, c)]), inv);
-          g.rr[swg(i, c)] = x.x;
-          g.ri[swg(i, c)] = x.y;
-          g.mr[swg(i, c)] = y.x;
-          g.mi[swg(i, c)] = y.y;
-          g.colq[buf][i] = x;
-          g.colq[buf][GB + i] = y;
-        }
+        const int i = lane & (GB - 1);
+        double* const vr = (lane < GB ? g.rr : g.mr) + swg(i, ct);
+        double* const vi = (lane < GB ? g.ri : g.mi) + swg(i, ct);
+        const double2 x = cmul(make_double2(*vr, *vi), inv);
+        *vr = x.x;
+        *vi = x.y;
+        g.colq[buf][lane] = x;  // [0, GB): R rows, [GB, 2 GB): M rows
       }
       if (__syncthreads_or(myfail)) break;
       if (c < np && c != ct) {
