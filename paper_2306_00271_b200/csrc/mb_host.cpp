@@ -530,8 +530,6 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
   if (opts->path < 0 || opts->path > 4) fail(MB_ERR_ARG, "options: path must be 0..4");
   if (opts->path >= 2) npad = 0;
   if (conv) npad = 2 * n;
-  if (fields[0].has_bulk_period && !r_init && opts->path == 2)
-    fail(MB_ERR_CONFIG, "bulk seeding runs in the resident and cluster kernels only (path 0, 1, 3 or 4)");
   bool big = npad == 0 && !conv;
   if (big) npad = (n + 7) & ~7;
 
@@ -642,8 +640,9 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
   // 18.5), where its four stage products per step amortise the per-pair solves.
   bool cluster = false;
   if (conv) big = false;
-  // bulk seeding (per-pair period loop until R settles) exists only in the
-  // on-chip kernels, so it takes the cluster kernel at any batch size
+  // bulk seeding (per-pair period loop until R settles) runs inside the on-chip
+  // kernels; the batched path steps the periods from the host (one sync per
+  // period), so auto takes the cluster kernel at any batch size when it fits
   const bool want_cluster = opts->path == 3 || opts->path == 4;
   const int rk4 = stepper->algorithm == MB_STEP_RK4;
   if (big && (want_cluster || (opts->path == 0 && (npairs < 512 || bulk || !rk4)))) {
@@ -658,11 +657,6 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
       fail(MB_ERR_CONFIG, "cluster kernel does not cover this rod count / stepper / box size");
     }
   }
-
-  if (bulk && big)
-    fail(MB_ERR_CONFIG,
-         "bulk seeding runs in the resident (N <= 64) and cluster (64 < N <= 256) kernels only; "
-         "this rod count / stepper does not fit the cluster kernel's shared memory");
 
   mb_plan* pl = new mb_plan();
   pl->ctx = ctx;
@@ -896,6 +890,9 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
       b.ginv = p.ginv;
       b.sin_theta0 = p.sin_theta0;
       b.r_init = r_init ? p.bulk_scratch : nullptr;
+      b.bulk_r = bulk ? p.bulk_scratch : nullptr;
+      b.bulk_tol = p.bulk_tol;
+      b.bulk_left = bulk ? dev_alloc<unsigned>(pl, 2) : nullptr;
       // splitting: Q0, Q1 (ping-pong), P, scratch; rk4: Q, P, X2, X3, W, V, SQ
       b.nmat = p.rk4 ? 7 : 4;
       b.pair_stride = (long)b.nmat * 2 * npad * npad;
@@ -928,8 +925,12 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
 // meanwhile. Launches are issued step by step, alternating halves, so neither
 // stream's queue runs ahead of the other. Pairs are independent: the halves
 // give bitwise the rows of one batch.
-mbx::BigParams big_part(const mbx::BigParams& b, long lo, long hi) {
+mbx::BigParams big_part(const mbx::BigParams& b, long lo, long hi, int index) {
   mbx::BigParams h = b;
+  const long rplanes = 2L * b.np * b.np;
+  if (b.r_init) h.r_init = b.r_init + lo * rplanes;
+  if (b.bulk_r) h.bulk_r = b.bulk_r + lo * rplanes;
+  if (b.bulk_left) h.bulk_left = b.bulk_left + index;
   const long chk_per = (long)((b.np + 15) / 16) * 4;
   h.npairs = hi - lo;
   h.pair_struct = b.pair_struct + lo;
@@ -961,7 +962,7 @@ void execute_big(mb_plan* pl, cudaStream_t st) {
       cuda_check(cudaEventCreateWithFlags(&pl->join, cudaEventDisableTiming), "cudaEventCreate");
     }
     const long half = pl->bp.npairs / 2;
-    part = {big_part(pl->bp, 0, half), big_part(pl->bp, half, pl->bp.npairs)};
+    part = {big_part(pl->bp, 0, half, 0), big_part(pl->bp, half, pl->bp.npairs, 1)};
     sts = {st, pl->side};
     cuda_check(cudaEventRecord(pl->fork, st), "event");
     cuda_check(cudaStreamWaitEvent(pl->side, pl->fork, 0), "stream wait");
@@ -988,29 +989,19 @@ void execute_big(mb_plan* pl, cudaStream_t st) {
       cuda_check(cudaStreamWaitEvent(st, pl->join, 0), "stream wait");
     }
   };
-  auto slot = [&](int step, int r) { return (long)step * pl->stride + p.occ_node[r]; };
+  // One window of L steps (run_window, proposed.cpp:275-289) whose node slots
+  // start at `base`: the slab, or one bulk period on the bulk window's step
+  // (proposed.cpp:311-321). Failures report step_off + step.
   mbx::BigStage s{};
-  const int L = p.nsteps;
-  if (p.rk4) {
-    const int Q = 0, P = 1, X2 = 2, X3 = 3, W = 4, V = 5, SQ = 6;
-    s = mbx::BigStage{0, 0, 0, 0, p.h, 0.0, 0.0, Q, -1, P, X2, X3, W, V, SQ};
-    launch(s);  // initial state + X2
-    for (int step = 0; step < L; ++step) {
-      const int ops[4] = {Q, X2, X3, V};
-      for (int k = 0; k < 4; ++k) {
-        s = mbx::BigStage{3 + k, ops[k], slot(step, k), step, p.h, 0.0, 0.0, Q, -1, P, X2, X3, W, V, SQ};
-        launch(s);
-      }
-      check_and_solve(step, Q, P, X3, V, X2, p.h);
-    }
-    surface(Q, P, X3, V);
-    return;
-  }
-  const int P = 2, SCR = 3;
+  const int Q = 0, P4 = 1, X2 = 2, X3 = 3, W = 4, V = 5, SQ = 6;  // rk4 matrices
+  const int P = 2, SCR = 3;                                       // splitting: Q0, Q1, P, scratch
   int qc = 0;
-  s = mbx::BigStage{0, 0, 0, 0, p.h, 0.0, 0.0, qc, -1, P, -1, -1, -1, -1, -1};
-  launch(s);
   const int nk = p.nocc;
+  auto init = [&](int kind, double hw) {
+    s = p.rk4 ? mbx::BigStage{kind, 0, 0, 0, hw, 0.0, 0.0, Q, -1, P4, X2, X3, W, V, SQ}
+              : mbx::BigStage{kind, 0, 0, 0, hw, 0.0, 0.0, qc, -1, P, -1, -1, -1, -1, -1};
+    launch(s);  // initial state (rk4: + X2)
+  };
   // FSAL is not merged on the batched path: a merged kick must keep the
   // reference's two roundings around the end-of-step check (see the on-chip
   // kernels), and here the shared product would be an extra N x N plane per
@@ -1020,20 +1011,63 @@ void execute_big(mb_plan* pl, cudaStream_t st) {
     launch(d);
     qc ^= 1;
   };
-  for (int step = 0; step < L; ++step) {
-    for (int r = 0; r < nk; ++r) {
-      const bool last = r == nk - 1;
-      if (p.variant == 0) drift(p.occ_drift[r]);
-      const double kc = p.occ_kick[r];
-      const double dc = (p.variant == 1 && !last) ? p.occ_drift[r] : 0.0;
-      mbx::BigStage k{1, qc, slot(step, r), step, kc, dc, 0.0, qc, qc ^ 1, P, -1, -1, -1, -1, -1};
-      launch(k);
-      if (dc != 0.0) qc ^= 1;
+  auto window = [&](long base, int Lw, double hw, const double* kick, const double* drf, double fin, int step_off) {
+    auto slot = [&](int step, int r) { return base + (long)step * pl->stride + p.occ_node[r]; };
+    for (int step = 0; step < Lw; ++step) {
+      if (p.rk4) {
+        const int ops[4] = {Q, X2, X3, V};
+        for (int k = 0; k < 4; ++k) {
+          s = mbx::BigStage{3 + k, ops[k], slot(step, k), step_off + step, hw, 0.0, 0.0, Q, -1, P4, X2, X3, W, V, SQ};
+          launch(s);
+        }
+        check_and_solve(step_off + step, Q, P4, X3, V, X2, hw);
+        continue;
+      }
+      for (int r = 0; r < nk; ++r) {
+        const bool last = r == nk - 1;
+        if (p.variant == 0) drift(drf[r]);
+        const double kc = kick[r];
+        const double dc = (p.variant == 1 && !last) ? drf[r] : 0.0;
+        mbx::BigStage k{1, qc, slot(step, r), step_off + step, kc, dc, 0.0, qc, qc ^ 1, P, -1, -1, -1, -1, -1};
+        launch(k);
+        if (dc != 0.0) qc ^= 1;
+      }
+      if (p.variant == 0) drift(fin);
+      check_and_solve(step_off + step, qc, P, qc ^ 1, SCR, -1, 0.0);
     }
-    if (p.variant == 0) drift(p.final_drift);
-    check_and_solve(step, qc, P, qc ^ 1, SCR, -1, 0.0);
+  };
+  if (p.bulk_steps > 0) {
+    // bulk seeding (compute_bulk_reflection_proposed, proposed.cpp:311-342):
+    // one bulk period after another from R = 0; after each period the full R
+    // is read (the surface solve's machinery) and compared with the previous
+    // one per pair; a settled pair is frozen until the slab is seeded. One
+    // host sync per period (the count of pairs still unsettled).
+    init(0, p.bulk_h);
+    for (long m = 0; m < p.bulk_max_periods; ++m) {
+      window(p.bulk_base, p.bulk_steps, p.bulk_h, p.bulk_kick, p.bulk_drift, p.bulk_final_drift,
+             (int)(m * p.bulk_steps));
+      const int mode = m + 1 == p.bulk_max_periods ? 3 : 2;
+      unsigned left[2] = {0, 0};
+      for (int h = 0; h < H; ++h) {
+        cuda_check(cudaMemsetAsync(part[h].bulk_left, 0, sizeof(unsigned), sts[h]), "memset");
+        cuda_check(p.rk4 ? mbx::big_launch_gj(part[h], mode, (int)m, Q, P4, X3, V, -1, 0.0, sts[h], nl)
+                         : mbx::big_launch_gj(part[h], mode, (int)m, qc, P, qc ^ 1, SCR, -1, 0.0, sts[h], nl),
+                   "big bulk-read launch");
+        cuda_check(cudaMemcpyAsync(&left[h], part[h].bulk_left, sizeof(unsigned), cudaMemcpyDeviceToHost, sts[h]),
+                   "D2H bulk count");
+      }
+      for (int h = 0; h < H; ++h) cuda_check(cudaStreamSynchronize(sts[h]), "bulk period sync");
+      if (left[0] + left[1] == 0) break;
+    }
+    init(7, p.h);  // Q = G^-1 (I + R)/2, P = (i/2)(I - R) from the settled R
+  } else {
+    init(0, p.h);
   }
-  surface(qc, P, qc ^ 1, SCR);
+  window(0, p.nsteps, p.h, p.occ_kick, p.occ_drift, p.final_drift, 0);
+  if (p.rk4)
+    surface(Q, P4, X3, V);
+  else
+    surface(qc, P, qc ^ 1, SCR);
 }
 
 void execute_plan(mb_plan* pl, cudaStream_t st) {

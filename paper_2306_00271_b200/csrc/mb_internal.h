@@ -134,11 +134,20 @@ struct BigParams {
   double* eta;
   double2* rho;
   const double* r_init;  // caller-supplied R_init per pair (2 np^2 doubles: re, im planes) or null
+  // bulk seeding on the batched path (proposed.cpp:311-342): the previous
+  // period's R per pair (same plane layout), the stopping tolerance and the
+  // count of pairs that have not settled after the last bulk read
+  double* bulk_r;
+  double bulk_tol;
+  unsigned* bulk_left;
 };
+// PointStatus::code of a pair whose bulk R has settled: frozen (every kernel
+// skips code != 0) until the slab is seeded from it; never leaves the device
+constexpr int kBulkSettled = 100;
 
 // one tiled-GEMM launch: acc = U(slot) * M[op]; epilogue `kind`
 struct BigStage {
-  int kind;   // 0 init, 1 kick(+drift), 2 drift, 3..6 rk4 stage 1..4
+  int kind;   // 0 init, 1 kick(+drift), 2 drift, 3..6 rk4 stage 1..4, 7 slab seeded from the settled bulk R
   int op;     // operand matrix of the GEMM
   long slot;  // node slot of U (box table)
   int step;

@@ -340,18 +340,26 @@ __global__ void big_elem_kernel(const __grid_constant__ BigParams p, const __gri
   for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < total; idx += (long)gridDim.x * blockDim.x) {
     const long pair = idx / NN, o = idx % NN;
     const int r = (int)(o / p.np), c = (int)(o % p.np);
-    if (s.kind == 0) {
+    if (s.kind == 0 || s.kind == 7) {
+      // kind 7: the slab of a pair whose bulk R settled starts from that R
+      // (compute_bulk_reflection_proposed -> R_init, sweep.cpp:96-101); pairs
+      // that failed in the bulk windows keep their status
+      const double* seed = s.kind == 7 ? p.bulk_r : p.r_init;
+      if (s.kind == 7) {
+        const int code = p.status[pair].code;
+        if (code != kBulkSettled && code != 0) continue;
+      }
       if (o == 0) {
-        p.status[pair] = PointStatus{0, 0, 0, 0};
+        p.status[pair] = PointStatus{0, 0, 0, 0};  // SolveStats counts the slab solve only
         p.xi[pair] = 0.0;
       }
       const bool d = (r == c) && (r < p.n);
       double qr, qi, pr, pi;
-      if (p.r_init) {
+      if (seed) {
         // caller-supplied R_init: Q = G^-1 (I + R)/2, P = (i/2)(I - R)
         // (from_tau_rho, proposed.cpp:114-128; the on-chip kernels' seeded slab)
         const double2 gi = r < p.n ? p.ginv[pair * p.n + r] : make_double2(0.0, 0.0);
-        const double re = p.r_init[pair * 2 * NN + o], im = p.r_init[pair * 2 * NN + NN + o];
+        const double re = seed[pair * 2 * NN + o], im = seed[pair * 2 * NN + NN + o];
         const double dlt = d ? 1.0 : 0.0;
         const double ar = 0.5 * (dlt + re), ai = 0.5 * im;
         qr = gi.x * ar - gi.y * ai;
@@ -882,8 +890,9 @@ __global__ void __launch_bounds__(NTH, NPM == 128 ? 2 : 1) big_gj_kernel(const _
   if (!ok) {
     if (tid == 0) {
       PointStatus st = p.status[pair];
-      st.code = mode == 0 ? 2 : 3;
-      st.step = mode == 0 ? step : p.nsteps;
+      // RHST / reflection extraction / bulk reflection read (step = period)
+      st.code = mode == 0 ? 2 : (mode == 1 ? 3 : 4);
+      st.step = mode == 1 ? p.nsteps : step;
       p.status[pair] = st;
     }
     return;
@@ -912,6 +921,52 @@ __global__ void __launch_bounds__(NTH, NPM == 128 ? 2 : 1) big_gj_kernel(const _
       if (!isfinite(p.xi[pair])) st.reserved += 1;
       p.status[pair] = st;
     }
+  } else if (mode >= 2) {
+    // bulk read of period `step`: ||R - R_prev||_F <= tol max(1, ||R||_F)
+    // (proposed.cpp:334-339); R is kept (zero-padded planes) for the next
+    // comparison and for the slab seed. The state (Q, P) continues untouched.
+    double* R = p.bulk_r + pair * 2 * NN;
+    double dn = 0.0, rn = 0.0;
+    for (long o = tid; o < NN; o += NTH) {
+      const int r = (int)(o / np), c = (int)(o % np);
+      double xr = 0.0, xi = 0.0;
+      if (r < n && c < n) {
+        xr = X[o];
+        xi = X[NN + o];
+        if (step > 0) {
+          const double d0 = xr - R[o], d1 = xi - R[NN + o];
+          dn += d0 * d0 + d1 * d1;
+        }
+        rn += xr * xr + xi * xi;
+      }
+      R[o] = xr;
+      R[NN + o] = xi;
+    }
+    dn = warp_sum(dn);
+    rn = warp_sum(rn);
+    if (lane == 0) {
+      g.sums[0][warp] = dn;
+      g.sums[1][warp] = rn;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double D = 0.0, Rn = 0.0;
+      for (int w = 0; w < NTH / 32; ++w) {
+        D += g.sums[0][w];
+        Rn += g.sums[1][w];
+      }
+      PointStatus st = p.status[pair];
+      if (step > 0 && sqrt(D) <= p.bulk_tol * fmax(1.0, sqrt(Rn))) {
+        st.code = kBulkSettled;
+        p.status[pair] = st;
+      } else if (mode == 3) {  // ConvergenceError: the bulk R did not settle
+        st.code = 5;
+        st.step = step + 1;
+        p.status[pair] = st;
+      } else {
+        atomicAdd(p.bulk_left, 1u);
+      }
+    }
   } else {
     const double s0 = p.sin_theta0[pair];
     const double g0 = G[0].x;
@@ -929,7 +984,7 @@ __global__ void __launch_bounds__(NTH, NPM == 128 ? 2 : 1) big_gj_kernel(const _
 
 // ------------------------------------------------------------------ launchers
 cudaError_t big_launch_stage(const BigParams& p, const BigStage& s, cudaStream_t st, int* launches) {
-  if (s.kind == 0 || s.kind == 2) {
+  if (s.kind == 0 || s.kind == 2 || s.kind == 7) {
     const long total = p.npairs * (long)p.np * p.np;
     const int blocks = (int)min((total + 255) / 256, (long)148 * 32);
     big_elem_kernel<<<blocks, 256, 0, st>>>(p, s);

@@ -126,7 +126,10 @@ int main(int argc, char** argv) {
         d = std::max(d, std::abs(rho0[(std::size_t)i] - a.rho[(std::size_t)(1 * a.rods + i)]));
         dz = std::max(dz, std::abs(rhoz[(std::size_t)i] - rho0[(std::size_t)i]));
       }
-      CHECK(d == 0.0 && dz == 0.0);
+      // the same pair in a 6-pair plan and alone; the zero-seeded solve runs the
+      // seeded (BULK) instantiation of the kernel: rounding-level agreement
+      if (!(d <= 1e-13 && dz <= 1e-13)) std::printf("solve_proposed: d = %.3e, dz = %.3e\n", d, dz);
+      CHECK(d <= 1e-13 && dz <= 1e-13);
       CHECK(stats.rhst_transforms == a.status[1].rhst_count);
       std::vector<Complex> seeded = zero;
       for (int i = 0; i < rods.size(); ++i) seeded[(std::size_t)(i * rods.size() + i)] = Complex(0.2, -0.1);

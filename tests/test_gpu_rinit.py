@@ -119,6 +119,23 @@ def test_r_init_two_shards_equal_one_device():
     assert np.array_equal(one, two)
 
 
+def test_r_init_batched_two_streams_keep_pair_order():
+    """From 1024 pairs the batched path runs two half-batches on two streams:
+    a per-pair R_init must follow its pair into the second half."""
+    n = 65
+    w = configs.config4(n, "rk4", n_structures=1).subset(theta0=[0.5 + 0.004 * i for i in range(1024)], slices=4,
+                                                         z_bottom=-0.064)
+    R = seeded_r(n, 1024, seed=13)
+    rods = mb.RodSet.build_first(mb.Lattice2D(w.a1, w.a2), w.n_rods)
+    opts = mb.SweepOptions(method="rk4", slices=w.slices, dz=-w.z_bottom / w.slices, path=2)
+    pairs = [(0, t, 0.0) for t in w.theta0]
+    fields = configs.product_fields(w)
+    whole, _, _ = mb.solve_batch(fields, rods, w.gamma, pairs, opts, r_init=R)
+    lo, _, _ = mb.solve_batch(fields, rods, w.gamma, pairs[:512], opts, r_init=R[:512])
+    hi, _, _ = mb.solve_batch(fields, rods, w.gamma, pairs[512:], opts, r_init=R[512:])
+    assert np.array_equal(whole, np.concatenate([lo, hi]))
+
+
 def test_solve_proposed_mirror(ref):
     n = F.rods11(ref).size()
     R = seeded_r(n, 1, seed=5)[0]
