@@ -88,9 +88,10 @@ typedef struct {
   int kind;
   double z_bottom; /* A, < 0 */
   int has_bulk_period; /* bulk seed R_init per pair (compute_bulk_reflection_proposed,
-                          proposed.cpp:311-342): resident kernel (N <= 64) and cluster
-                          kernel (64 < N <= 256; rk4 only up to N = 128); other
-                          cases return MB_ERR_CONFIG. A caller-supplied R_init
+                          proposed.cpp:311-342), every N <= 256 and stepper: inside
+                          the resident (N <= 64) and cluster kernels (64 < N <= 256;
+                          rk4 up to N = 128), on the batched path otherwise (bulk
+                          periods stepped from the host). A caller-supplied R_init
                           (mb_plan_create_seeded) replaces it. */
   double bulk_period;
   /* MB_FIELD_GAUSSIAN_LAYERS: layers[nlayers][5] = z_center, amplitude,

@@ -48,6 +48,8 @@ CASES = {
     "bulk_n81_rk4": lambda: _bulk(81, "rk4"),
     "bulk_n67_sp6": lambda: _bulk(67, "sp6"),
     "bulk_n143_sp6": lambda: _bulk(143, "sp6"),
+    # rk4 above 128 rods: the batched path's bulk seed (the cluster kernel's third slab plane does not fit)
+    "bulk_n143_rk4": lambda: _bulk(143, "rk4"),
 }
 
 

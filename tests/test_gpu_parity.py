@@ -323,32 +323,24 @@ def test_bulk_atoms_parity(ref, oracle, method):
     H.assert_parity(eta, want, H.run_oracle(oracle, w, threads=4, method=method)[0])
 
 
-@pytest.mark.parametrize("n,method,path", [(255, "rk4", 0), (127, "sp6", 2), (81, "rk4", 2)])
-def test_bulk_batched_parity(ref, n, method, path):
-    """Bulk seeding on the batched path (state in HBM, the periods stepped from
-    the host): rk4 at N > 128 does not fit the cluster kernel, so auto takes
-    this path; path 2 forces it elsewhere."""
-    w = configs.config4(n, method, n_structures=1).subset(theta0=[0.9, 2.7], slices=100)
-    w.bulk_period = 3.13  # one 0.78 + 2.35 A layer pair, continued below z_bottom
-    want, _, rh = H.run_oracle(ref, w, threads=8, method=method)
-    eta, _, st = H.run_device(w, method=method, path=path)
-    assert (st["code"] == 0).all()
-    assert np.array_equal(st["rhst"], rh)
-    assert H.curve_err(eta, want) <= TOL
+# Bulk seeding on the batched path (state in HBM, the bulk periods stepped
+# from the host with one sync per period): rk4 at N > 128 does not fit the
+# cluster kernel, so auto takes this path; path 2 forces it elsewhere.
+@pytest.mark.parametrize("method", ["rk4", "sp4", "sp6"])
+def test_bulk_batched_layered_parity(ref, method):
+    t0 = [2.0, 7.0, 15.0]
+    of = ref.PotentialField.gaussian_layers(-10.0, F.LAYERED_LAYERS, 5.0)
+    rc = oracle_curve(ref, of, F.rods11(ref), F.K_GAMMA11, t0, method, 0.05)
+    field = mb.PotentialField.gaussian_layers(-10.0, F.LAYERED_LAYERS, bulk_period=5.0)
+    c = mb.rocking_curve(field, dev_rods11(), F.K_GAMMA11, mb.AngleGrid.validated(t0, [0.0]),
+                         mb.SweepOptions(method=method, dz=0.05, path=2))
+    assert np.array_equal(c.status["rhst"], rc.rhst)
+    assert H.curve_err(c.eta, rc.eta) <= TOL
     # R_bulk is defined only to its stopping rule (proposed.cpp:334-339), as in
     # test_bulk_layered_parity
-    assert H.entry_rel_err(eta, want, floor=1e-6) <= 1e-8
-    assert H.entry_rel_err(eta, want, floor=1e-10) <= 1e-7
-
-
-def test_bulk_batched_matches_cluster():
-    w = configs.config4(127, "sp6", n_structures=1).subset(theta0=[0.9, 2.7, 4.4], slices=100)
-    w.bulk_period = 3.13
-    a, _, sa = H.run_device(w, path=2)
-    b, _, sb = H.run_device(w, path=4)
-    assert (sa["code"] == 0).all() and (sb["code"] == 0).all()
-    assert np.array_equal(sa["rhst"], sb["rhst"])
-    assert H.curve_err(a, b) <= TOL
+    assert H.entry_rel_err(c.eta, rc.eta, floor=1e-6) <= 1e-8
+    assert H.entry_rel_err(c.eta, rc.eta, floor=1e-10) <= 1e-7
+    assert H.entry_abs_err(c.eta, rc.eta) <= 1e-11
 
 
 # FSAL shares one product W between the last kick of a step and the first
