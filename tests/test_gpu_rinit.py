@@ -102,6 +102,45 @@ def test_r_init_large_designs_parity(ref, oracle, n_rods, method, path):
     assert H.entry_rel_err(eta, rc.eta) <= (TOL if n_rods < 255 else 1e-8)
 
 
+def shifted_r(n, count, shift=3, weight=1.5, seed=17):
+    """R = weight * (cyclic shift) + small noise: in Q = G^-1 (I + R)/2 every
+    row's largest entry sits `shift` columns off the diagonal, so the first
+    RHST takes an off-diagonal pivot in every row of every panel."""
+    R = seeded_r(n, count, seed=seed, scale=0.2)
+    for i in range(n):
+        R[:, i, (i + shift) % n] += weight
+    return R
+
+
+@pytest.mark.parametrize("n_rods,path", [(31, 1), (61, 1), (81, 3), (81, 4), (81, 2), (143, 4)])
+def test_off_diagonal_pivots_take_the_pivoting_solves(ref, n_rods, path):
+    """The speculative diagonal-pivot factorisations (resident verified blocks,
+    the cluster kernel's fast panel factorisation, the batched path's
+    diagonal pass) must fall back to the first-maximum pivot chain: a seeded
+    state whose row maxima are off the diagonal, RHST threshold 0 (a
+    transform after every step; the first one pivots off the diagonal
+    everywhere, the later ones start from Q = I)."""
+    w = configs.config4(n_rods, "sp6", n_structures=1).subset(theta0=[0.8, 2.3, 4.1], slices=12, z_bottom=-0.192)
+    R = shifted_r(n_rods, len(w.theta0))
+    rods_r = ref.RodSet.build_first(H.oracle_lattice(ref, w), w.n_rods)
+    opts_r = ref.SweepOptions()
+    opts_r.method, opts_r.dz, opts_r.threads, opts_r.slices = "sp6", -w.z_bottom / w.slices, 4, w.slices
+    opts_r.rhst_threshold = 0.0
+    opts_r.set_r_init(R)
+    rc = ref.rocking_curve(H.oracle_fields(ref, w)[0], rods_r, w.gamma, ref.AngleGrid.validated(list(w.theta0), [0.0]),
+                           opts_r)
+    rods = mb.RodSet.build_first(mb.Lattice2D(w.a1, w.a2), w.n_rods)
+    opts = mb.SweepOptions(method="sp6", slices=w.slices, dz=-w.z_bottom / w.slices, rhst_threshold=0.0, path=path)
+    eta, _, st = mb.solve_batch(configs.product_fields(w), rods, w.gamma, [(0, t, 0.0) for t in w.theta0], opts,
+                                r_init=R)
+    assert (st["code"] == 0).all()
+    assert np.array_equal(st["rhst"], rc.rhst) and (rc.rhst == w.slices).all()
+    assert (st["rhst_pivoting"] >= 1).all()
+    assert H.curve_err(eta, rc.eta) <= TOL
+    assert H.entry_rel_err(eta, rc.eta, floor=1e-6) <= TOL
+    assert H.entry_rel_err(eta, rc.eta) <= 1e-8
+
+
 def test_r_init_two_shards_equal_one_device():
     """Per-pair R_init follows its pair through the multi-device gather."""
     t0 = [2.0, 5.0, 9.0, 14.0, 20.0]
