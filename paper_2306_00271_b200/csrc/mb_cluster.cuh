@@ -993,6 +993,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
     unsigned* smask = reinterpret_cast<unsigned*>(pslot + SW);  // [NP/32] special-column bitmask
     int* sn = reinterpret_cast<int*>(smask + NP / 32);          // [1] special count
     int* lpp = sn + 1;                                          // [16] pivot columns
+    int* sdiag = lpp + SW;                                      // [1] every pivot of the panel is its diagonal
     double2* fs = tloc + 8 * SW;                                // [16][32] F on special columns
     double2* linv = fs + 2 * SW * SW;                           // [16] 1/pivot
     double* lpv = reinterpret_cast<double*>(linv + SW);         // [16] |pivot|^2
@@ -1011,13 +1012,37 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
       double* Xi = isA ? Ai_ : Bi_;
       const bool act = gi < n && (isA ? gi >= p0 + SW : true);
       // (A) sequential ops on the special columns
+      double2 xk[SW];
+      if (TPR == SW && sdiag[0]) {
+        // all-diagonal panel (the common case): the special columns are the
+        // panel's own 16, slot = column, p_k = k. One value per thread, one
+        // broadcast per op; bitwise the general form below.
+        const int j = p0 + cg;
+        double2 v = act ? make_double2(Xr[sw<NP>(lr, j)], Xi[sw<NP>(lr, j)]) : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int lk = 0; lk < SW; ++lk) {
+          xk[lk] = make_double2(0.0, 0.0);
+          if (lk < nk) {
+            const double2 xp = make_double2(__shfl_sync(0xffffffffu, v.x, rbase | lk),
+                                            __shfl_sync(0xffffffffu, v.y, rbase | lk));
+            const double2 x = cmul(xp, linv[lk]);
+            xk[lk] = x;
+            const double2 f = fs[lk * 2 * SW + cg];
+            const double2 nv = make_double2(v.x - (f.x * x.x - f.y * x.y), v.y - (f.x * x.y + f.y * x.x));
+            v = (cg == lk) ? x : nv;
+          }
+        }
+        if (act) {
+          Xr[sw<NP>(lr, j)] = v.x;
+          Xi[sw<NP>(lr, j)] = v.y;
+        }
+      } else {
       double2 val[SLOTS];
 #pragma unroll
       for (int u = 0; u < SLOTS; ++u) {
         const int j = scol[cg + TPR * u];
         val[u] = (act && j >= 0) ? make_double2(Xr[sw<NP>(lr, j)], Xi[sw<NP>(lr, j)]) : make_double2(0.0, 0.0);
       }
-      double2 xk[SW];
 #pragma unroll
       for (int lk = 0; lk < SW; ++lk) {
         xk[lk] = make_double2(0.0, 0.0);
@@ -1054,6 +1079,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
             Xi[sw<NP>(lr, j)] = val[u].y;
           }
         }
+      }
       }
       CPROF(7);  // special columns
       // (B) other columns: X[i][j] -= sum_k x_k(i) F_k[j] (F_k[j] = A[k][j])
@@ -1175,7 +1201,11 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
         if (lane < SW && p0 + lane < NP) atomicOr(&smask[(p0 + lane) >> 5], 1u << ((p0 + lane) & 31));
         if (first) atomicOr(&smask[pk >> 5], 1u << (pk & 31));
         const bool anybad = __any_sync(FULL, bad);
-        if (lane == 0) sn[0] = anybad ? -1 : cnt;
+        const bool alldiag = __all_sync(FULL, !has || pk == p0 + lane);
+        if (lane == 0) {
+          sn[0] = anybad ? -1 : cnt;
+          sdiag[0] = alldiag ? 1 : 0;
+        }
       }
       __syncthreads();
       if (sn[0] < 0) {  // zero pivot: the same owner data everywhere
