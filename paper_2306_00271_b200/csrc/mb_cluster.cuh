@@ -1171,6 +1171,15 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
       const double2* rt = peer(tpub, b);
       war = M2r + (long)p0 * NP;
       wai = M2i + (long)p0 * NP;
+      // F on the panel's own 16 columns, fetched together with the pivot
+      // table on the guess that every pivot is the diagonal (one L2 round
+      // trip fewer on the chain; the general gather below otherwise)
+      double2 fspec = make_double2(0.0, 0.0);
+      if (SW * SW <= CNT && tid < SW * SW) {
+        const int lk = tid / SW, c = tid % SW;
+        if (lk < nk && p0 + c < n && c != lk)
+          fspec = make_double2(__ldcg(war + (long)lk * NP + p0 + c), __ldcg(wai + (long)lk * NP + p0 + c));
+      }
       if (tid < SW) {
         linv[tid] = pld(rt + tid);
         lpp[tid] = pld(reinterpret_cast<const int*>(rt + 2 * SW) + tid);
@@ -1213,6 +1222,12 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
         break;
       }
       // F restricted to special columns: fs[lk][s]
+      if (SW * SW <= CNT && sdiag[0]) {
+        if (tid < SW * SW) {
+          fs[(tid / SW) * 2 * SW + tid % SW] = fspec;
+          fs[(tid / SW) * 2 * SW + SW + tid % SW] = make_double2(0.0, 0.0);
+        }
+      } else
       for (int w = tid; w < SW * 2 * SW; w += CNT) {
         const int lk = w / (2 * SW), sl = w % (2 * SW);
         const int j = scol[sl];
