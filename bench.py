@@ -52,7 +52,7 @@ UNIT = "points/s"
 HEADLINE = 3
 LEGS = (1, 2)
 # committed ncu --set full summaries of the propagation kernel per workload
-NCU = {3: "ncu_summary_r02ae_cfg3.json", 1: "ncu_summary_r01ab.json", 2: "ncu_summary_r01i_cfg2.json"}
+NCU = {3: "ncu_summary_r02ag_cfg3.json", 1: "ncu_summary_r01ab.json", 2: "ncu_summary_r01i_cfg2.json"}
 
 
 def dist_env():

@@ -507,7 +507,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
           asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(gbar) : "memory");
           if ((int)(v - target) >= 0) break;
           if (++spins > (1L << 28)) __trap();  // a group that never assembles: abort, never hang
-          __nanosleep(64);
+          __nanosleep(20);
         }
         asm volatile("fence.acq_rel.gpu;" ::: "memory");
       }
@@ -972,7 +972,7 @@ __global__ void __launch_bounds__(CNT, C::MINB) cluster_kernel(const __grid_cons
           asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(fa) : "memory");
           if (v == sid) break;
           if (++spins > (1L << 28)) __trap();
-          __nanosleep(64);
+          __nanosleep(20);
         }
         asm volatile("fence.acq_rel.gpu;" ::: "memory");
       } else {
