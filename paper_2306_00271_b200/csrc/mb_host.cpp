@@ -27,6 +27,8 @@
 #include "../../include/manybeam_b200.h"
 #include "mb_internal.h"
 
+constexpr int kBigParts = 4;  // batched path: most sub-batches (streams) of one execute
+
 namespace {
 
 using cd = std::complex<double>;
@@ -437,8 +439,9 @@ struct mb_plan {
   mbx::PotentialParams pot{};
   mbx::PropagateParams prop{};
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
-  cudaStream_t side = nullptr;  // batched path: second half-batch stream
-  cudaEvent_t fork = nullptr, join = nullptr;
+  std::vector<cudaStream_t> sides;  // batched path: streams of the other sub-batches
+  std::vector<cudaEvent_t> joins;
+  cudaEvent_t fork = nullptr;
   float ms_total = 0, ms_pot = 0, ms_prop = 0;
   int launches = 0;
   long h2d_bytes = 0;
@@ -485,8 +488,8 @@ void free_plan(mb_plan* pl) {
   for (cudaEvent_t& e : pl->ev)
     if (e) cudaEventDestroy(e);
   if (pl->fork) cudaEventDestroy(pl->fork);
-  if (pl->join) cudaEventDestroy(pl->join);
-  if (pl->side) cudaStreamDestroy(pl->side);
+  for (cudaEvent_t e : pl->joins) cudaEventDestroy(e);
+  for (cudaStream_t q : pl->sides) cudaStreamDestroy(q);
   delete pl;
 }
 
@@ -892,7 +895,7 @@ mb_plan* create_plan(mb_context* ctx, const mb_rods* rods, const mb_field* field
       b.r_init = r_init ? p.bulk_scratch : nullptr;
       b.bulk_r = bulk ? p.bulk_scratch : nullptr;
       b.bulk_tol = p.bulk_tol;
-      b.bulk_left = bulk ? dev_alloc<unsigned>(pl, 2) : nullptr;
+      b.bulk_left = bulk ? dev_alloc<unsigned>(pl, kBigParts) : nullptr;
       // splitting: Q0, Q1 (ping-pong), P, scratch; rk4: Q, P, X2, X3, W, V, SQ
       b.nmat = p.rk4 ? 7 : 4;
       b.pair_stride = (long)b.nmat * 2 * npad * npad;
@@ -951,21 +954,34 @@ mbx::BigParams big_part(const mbx::BigParams& b, long lo, long hi, int index) {
 void execute_big(mb_plan* pl, cudaStream_t st) {
   const mbx::PropagateParams& p = pl->prop;
   int* nl = &pl->launches;
-  // two halves from 1024 pairs (each half still fills the GPU with tiles)
-  const bool two = pl->bp.npairs >= 1024;
+  // sub-batches on their own streams: two from 1024 pairs, MB_BIG_PARTS (2..4,
+  // default 2) from 2048 (each part still fills the GPU with tiles)
+  int want = 1;
+  if (pl->bp.npairs >= 1024) want = 2;
+  if (pl->bp.npairs >= 2048) {
+    const char* e = std::getenv("MB_BIG_PARTS");
+    if (e) want = std::max(1, std::min(kBigParts, std::atoi(e)));
+  }
+  const bool two = want > 1;
   std::vector<mbx::BigParams> part;
   std::vector<cudaStream_t> sts;
   if (two) {
-    if (!pl->side) {
-      cuda_check(cudaStreamCreateWithFlags(&pl->side, cudaStreamNonBlocking), "cudaStreamCreate");
-      cuda_check(cudaEventCreateWithFlags(&pl->fork, cudaEventDisableTiming), "cudaEventCreate");
-      cuda_check(cudaEventCreateWithFlags(&pl->join, cudaEventDisableTiming), "cudaEventCreate");
+    if (!pl->fork) cuda_check(cudaEventCreateWithFlags(&pl->fork, cudaEventDisableTiming), "cudaEventCreate");
+    while ((int)pl->sides.size() < want - 1) {
+      cudaStream_t q;
+      cudaEvent_t e;
+      cuda_check(cudaStreamCreateWithFlags(&q, cudaStreamNonBlocking), "cudaStreamCreate");
+      pl->sides.push_back(q);
+      cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+      pl->joins.push_back(e);
     }
-    const long half = pl->bp.npairs / 2;
-    part = {big_part(pl->bp, 0, half, 0), big_part(pl->bp, half, pl->bp.npairs, 1)};
-    sts = {st, pl->side};
     cuda_check(cudaEventRecord(pl->fork, st), "event");
-    cuda_check(cudaStreamWaitEvent(pl->side, pl->fork, 0), "stream wait");
+    for (int h = 0; h < want; ++h) {
+      const long lo = pl->bp.npairs * h / want, hi = pl->bp.npairs * (h + 1) / want;
+      part.push_back(big_part(pl->bp, lo, hi, h));
+      sts.push_back(h == 0 ? st : pl->sides[(std::size_t)h - 1]);
+      if (h > 0) cuda_check(cudaStreamWaitEvent(sts.back(), pl->fork, 0), "stream wait");
+    }
   } else {
     part = {pl->bp};
     sts = {st};
@@ -984,9 +1000,9 @@ void execute_big(mb_plan* pl, cudaStream_t st) {
     for (int h = 0; h < H; ++h)
       cuda_check(mbx::big_launch_gj(part[h], 1, p.nsteps, mq, mp, msa, msb, -1, 0.0, sts[h], nl),
                  "big surface-solve launch");
-    if (two) {
-      cuda_check(cudaEventRecord(pl->join, pl->side), "event");
-      cuda_check(cudaStreamWaitEvent(st, pl->join, 0), "stream wait");
+    for (int h = 1; h < H; ++h) {
+      cuda_check(cudaEventRecord(pl->joins[(std::size_t)h - 1], sts[h]), "event");
+      cuda_check(cudaStreamWaitEvent(st, pl->joins[(std::size_t)h - 1], 0), "stream wait");
     }
   };
   // One window of L steps (run_window, proposed.cpp:275-289) whose node slots
@@ -1047,7 +1063,7 @@ void execute_big(mb_plan* pl, cudaStream_t st) {
       window(p.bulk_base, p.bulk_steps, p.bulk_h, p.bulk_kick, p.bulk_drift, p.bulk_final_drift,
              (int)(m * p.bulk_steps));
       const int mode = m + 1 == p.bulk_max_periods ? 3 : 2;
-      unsigned left[2] = {0, 0};
+      unsigned left[kBigParts] = {0, 0, 0, 0};
       for (int h = 0; h < H; ++h) {
         cuda_check(cudaMemsetAsync(part[h].bulk_left, 0, sizeof(unsigned), sts[h]), "memset");
         cuda_check(p.rk4 ? mbx::big_launch_gj(part[h], mode, (int)m, Q, P4, X3, V, -1, 0.0, sts[h], nl)
@@ -1057,7 +1073,7 @@ void execute_big(mb_plan* pl, cudaStream_t st) {
                    "D2H bulk count");
       }
       for (int h = 0; h < H; ++h) cuda_check(cudaStreamSynchronize(sts[h]), "bulk period sync");
-      if (left[0] + left[1] == 0) break;
+      if (left[0] + left[1] + left[2] + left[3] == 0) break;
     }
     init(7, p.h);  // Q = G^-1 (I + R)/2, P = (i/2)(I - R) from the settled R
   } else {
